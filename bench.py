@@ -1,0 +1,325 @@
+"""Benchmark of the acoustic hot path on B200 (driver contract).
+
+One bench "step" = one complete BASELINE config-2 simulation at space order 8:
+a 512^3 grid with the smooth random model, sponge, 15 Hz Ricker source and
+512 receivers, advanced n_t = 500 time steps from zeroed levels (the zeroing
+is inside the step).  `value` = whole-job grid-point updates per second
+(GPts/s) with inputs resident in HBM; `e2e` = the same metric through the
+public host-buffer API (HostSimulation -> fdr_acoustic_run_host), with the
+H2D upload of m / sponge / series / receivers and the D2H download of the
+final wavefield and traces inside the timed region.  Inputs (2.1 GB of
+levels + m) exceed the 126 MB L2, so no flush is needed between steps.
+
+--impl reference times the reference's CPU algorithm (the oracle port of
+fdroof.kernel.step, numpy ufuncs with x-slab threads = host cores) on the
+same config: one bench step = one time step of the 512^3 grid.
+
+Multi-GPU: replicas only: every rank runs its own independent
+simulation; the timed region is bracketed by barriers, the time is the max
+over ranks and `value` sums all ranks' updates ("scaling": "weak").
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "GPts/s (grid-point updates/sec) and % of roofline per space order, 1 B200"
+UNIT = "GPts/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--order", type=int, default=8)
+    p.add_argument("--grid", type=int, default=512)
+    p.add_argument("--nt", type=int, default=500)
+    p.add_argument("--variant", default="auto")
+    p.add_argument("--no-sweep", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-steps", type=int, default=2)
+    return p.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reference_arm(args):
+    """CPU reference algorithm (oracle port of fdroof.kernel.step) on rank 0."""
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return 0
+    from oracle import acoustic as O
+    from paper_1608_03984_b200.synthetic import config2
+
+    cores = len(os.sched_getaffinity(0))
+    dims = (args.grid,) * 3
+    cfg = config2(order=args.order, n_t=args.nt, dims=dims)
+    st = O.OracleState(cfg.dims, cfg.halo)
+    taper = O.sponge_taper(cfg)
+    st.traces = np.zeros((cfg.n_t, cfg.receivers.count), np.float32)
+    for _ in range(args.warmup):
+        O.step(st, cfg, slabs=cores, taper=taper)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.step(st, cfg, slabs=cores, taper=taper)
+    wall = time.perf_counter() - t0
+    pts = float(np.prod(dims))
+    value = pts * args.steps / wall / 1e9
+    sample = (f"{args.steps} timed time-steps (after {args.warmup} warm-up) of the "
+              f"{dims[0]}^3 order-{args.order} update, numpy port of fdroof.kernel.step, "
+              f"slabs={cores}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded smooth random model, BASELINE config 2)",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args):
+    return {"workload": f"acoustic order {args.order}, {args.grid}^3, {args.nt} time steps "
+                        "(BASELINE config 2: smooth random model, sponge, Ricker, receivers)",
+            "grid": [args.grid] * 3, "order": args.order, "n_t": args.nt, "h_m": 10.0,
+            "l2": "inputs 4 x 0.54 GB > 126 MB L2 (no flush needed)",
+            "parallelism": "replicas" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "single"}
+
+
+def cpu_baseline(args, cfg):
+    from oracle import acoustic as O
+
+    cores = len(os.sched_getaffinity(0))
+    st = O.OracleState(cfg.dims, cfg.halo)
+    taper = O.sponge_taper(cfg)
+    O.step(st, cfg, slabs=cores, taper=taper)  # warm
+    t0 = time.perf_counter()
+    for _ in range(args.cpu_steps):
+        O.step(st, cfg, slabs=cores, taper=taper)
+    wall = time.perf_counter() - t0
+    value = float(np.prod(cfg.dims)) * args.cpu_steps / wall / 1e9
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{args.cpu_steps} time steps of the {cfg.dims[0]}^3 order-{cfg.order} "
+                      "update (numpy port of fdroof.kernel.step, x-slab threads)"}
+
+
+def load_ncu_traffic(order):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path, encoding="utf-8") as fh:
+            return json.load(fh).get(f"order{order}")
+    except (OSError, ValueError):
+        return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import torch
+
+    import paper_1608_03984_b200 as B
+    from paper_1608_03984_b200 import _lib
+    from paper_1608_03984_b200.synthetic import config2
+
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    lib = _lib.load()
+
+    dims = (args.grid,) * 3
+    cfg = config2(order=args.order, n_t=args.nt, dims=dims)
+    npts = float(np.prod(dims))
+    fld = B.Wavefield.allocate(cfg.dims, cfg.halo, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_sim(c=cfg, f=fld):
+        for g in f.grids:
+            g.zero_()
+        f.it = 0
+        B.run(f, c, variant=args.variant)
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        one_sim()
+    launches_per_sim = int(lib.fdr_last_launch_count())
+    barrier()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for _ in range(args.steps):
+            one_sim()
+        t_end.record(stream)
+        t_end.synchronize()
+    barrier()
+    ms = t_start.elapsed_time(t_end)
+    if pg is not None:
+        t = torch.tensor([ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+    per_rank_pts = npts * cfg.n_t * args.steps
+    value = world * per_rank_pts / (ms / 1e3) / 1e9
+
+    from paper_1608_03984_b200 import roofline as RL
+
+    peaks = RL.measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", RL.FALLBACK_HBM_GBS))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    launch_ms = ms / (args.steps * cfg.n_t)
+    achieved = npts * RL.ACOUSTIC_BYTES_PER_POINT / (launch_ms / 1e3) / 1e9
+    traffic = load_ncu_traffic(args.order)
+
+    # e2e through the public host-buffer API
+    e2e = None
+    if not args.no_e2e:
+        sim = B.HostSimulation(cfg, variant=args.variant, device=dev)
+        sim.run()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            sim.run()
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if pg is not None:
+            t = torch.tensor([ems], device=dev)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": world * per_rank_pts / (ems / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": sim.h2d_bytes, "d2h_bytes_per_step": sim.d2h_bytes,
+               "ms_per_step": ems / args.steps}
+        del sim
+
+    # per-order sweep (config 2 is a sweep over orders 2..16)
+    sweep = []
+    if not args.no_sweep:
+        for order in (2, 4, 8, 12, 16):
+            c = B.KernelConfig(order=order, dims=cfg.dims, n_t=cfg.n_t, dt=cfg.dt, h=cfg.h, m=cfg.m,
+                               source=cfg.source, receivers=cfg.receivers, sponge=cfg.sponge)
+            f = B.Wavefield.allocate(c.dims, c.halo, device=dev)
+            one_sim(c, f)
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            one_sim(c, f)
+            b.record(stream)
+            b.synchronize()
+            sms = a.elapsed_time(b)
+            g = npts * c.n_t / (sms / 1e3) / 1e9
+            sweep.append({"order": order, "gpts_per_s": round(g, 3),
+                          "achieved_gbs": round(g * 16, 1), "frac_hbm": round(g * 16 / hbm, 4),
+                          "flops_per_pt": RL.acoustic_flops_per_point(order),
+                          "gflops": round(g * RL.acoustic_flops_per_point(order), 1)})
+            del f
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args, cfg)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded smooth random model, BASELINE config 2)",
+            "config": workload_config(args),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": traffic,
+                         "peak_source": peak_src,
+                         "kernel": f"acoustic_tma<R={args.order // 2}> (one launch per time step)",
+                         "bytes_per_launch": int(npts * 16), "launch_ms": round(launch_ms, 5)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_sim * args.steps,
+            "clocks": clk.summary(),
+            "per_order": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,28 @@
+"""paper_1608_03984_b200: B200-native time stepping for the fdroof stencil hot path.
+
+Re-exports the reference's kernel API (/root/reference/pkg/src/fdroof/
+__init__.py:63-74: BenchResult, KernelConfig, Source, StabilityWarning,
+Wavefield, dump_wavefield, max_stable_dt, run_benchmark, step) backed by the
+sm_100a library libb200fd.so, plus the extensions the BASELINE configs need.
+"""
+
+from .errors import DeviceError, ExtensionMissingError, FdroofError, ValidationError
+from .kernel import (
+    BenchResult,
+    HostSimulation,
+    KernelConfig,
+    Receivers,
+    Source,
+    Sponge,
+    StabilityWarning,
+    Wavefield,
+    dump_wavefield,
+    max_stable_dt,
+    run,
+    run_benchmark,
+    step,
+)
+from .roofline import MachineSpec, RooflinePoint, b200_machine, roofline_point
+from .stencils import a2_sum, acoustic_weights_f32, second_derivative_weights
+
+__version__ = "0.1.0"

@@ -1,0 +1,102 @@
+// Shared device helpers for the b200fd kernels (sm_100a).
+//
+// Exact-arithmetic helpers: the reference computes with numpy float32 ufuncs
+// (/root/reference/pkg/src/fdroof/kernel.py:199-211), i.e. one IEEE
+// round-to-nearest rounding per operation and never a fused multiply-add.
+// The __f*_rn intrinsics are never contracted by nvcc, so every helper below
+// emits exactly one rounding per reference operation.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define FDR_DEV __device__ __forceinline__
+
+namespace fdr {
+
+// lap + w * (a + b): one tap pair of kernel.py:205 (three roundings).
+FDR_DEV float tap(float lap, float w, float a, float b) {
+  return __fadd_rn(lap, __fmul_rn(w, __fadd_rn(a, b)));
+}
+
+// (2c - prev) + s: kernel.py:211.  2*c == c + c exactly in IEEE arithmetic.
+FDR_DEV float leapfrog(float c, float prev, float s) {
+  return __fadd_rn(__fsub_rn(__fadd_rn(c, c), prev), s);
+}
+
+// ---------------------------------------------------------------- mbarrier
+FDR_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+FDR_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+FDR_DEV void mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+FDR_DEV void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+FDR_DEV void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+FDR_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+FDR_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// 3D TMA tile load global -> shared, completing on `bar` (complete_tx bytes).
+// Coordinates are element indices (z, y, x) and may be negative / beyond the
+// extents: those elements are zero-filled, which is the reference's
+// zero-Dirichlet halo (kernel.py:5-6).
+FDR_DEV void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                         int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+FDR_DEV void prefetch_tensormap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// Streaming (read-once) 16-byte global load that does not allocate in L1.
+FDR_DEV float4 ldg_stream(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// Streaming 16-byte store (evict-first).
+FDR_DEV void stg_stream(float* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+FDR_DEV float4 lds128(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+}  // namespace fdr

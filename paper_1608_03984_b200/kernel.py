@@ -1,0 +1,554 @@
+"""Acoustic leapfrog time stepping on one B200, behind the reference's kernel API.
+
+Drop-in for /root/reference/pkg/src/fdroof/kernel.py: the same `KernelConfig`,
+`Source`, `Wavefield`, `step`, `run_benchmark`, `max_stable_dt`,
+`dump_wavefield` and `StabilityWarning` names, argument meanings and error
+behaviour, but the wavefield lives in HBM and every step is one launch of the
+sm_100a kernel in libb200fd.so (ctypes, include/b200fd.h).  Extensions the
+BASELINE configs need and the reference lacks (SURVEY.md §8(a')): an
+absorbing `Sponge`, `Receivers` with recorded traces, and `run` for many steps
+per library call.
+
+Results are bit-identical to the reference's numpy float32 path: the kernel
+performs the reference's operations in the reference's order with one IEEE
+rounding each (kernel.py:199-211).  There is no CPU fallback.
+"""
+
+import ctypes
+import math
+import warnings
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import ValidationError
+from .roofline import (
+    ACOUSTIC_BYTES_PER_POINT,
+    MachineSpec,
+    RooflinePoint,
+    acoustic_flops_per_point,
+    b200_machine,
+    roofline_point,
+)
+from .stencils import abs_sum, acoustic_weights_f32, second_derivative_weights
+
+_VARIANTS = {"auto": _lib.VARIANT_AUTO, "direct": _lib.VARIANT_DIRECT, "tma": _lib.VARIANT_TMA}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class StabilityWarning(UserWarning):
+    """Configured time step exceeds the CFL bound (kernel.py:31-32)."""
+
+
+def max_stable_dt(order: int, h: float, m=1.0) -> float:
+    """CFL bound h*sqrt(4/a2)/v_max with a2 = 3*sum|w| (kernel.py:35-46)."""
+    a2 = float(3 * abs_sum(second_derivative_weights(order)))
+    m_min = float(np.min(m))
+    if m_min <= 0:
+        raise ValidationError("squared slowness must be positive")
+    return h * math.sqrt(4.0 / a2) / (1.0 / math.sqrt(m_min))
+
+
+@dataclass(frozen=True)
+class Source:
+    """Point source: additive time series injected at one interior point (kernel.py:49-54)."""
+
+    location: tuple
+    series: np.ndarray
+
+
+@dataclass(frozen=True)
+class Receivers:
+    """On-grid receivers: traces[it, i] = u_new[locations[i]] after injection."""
+
+    locations: np.ndarray
+
+    def __post_init__(self):
+        loc = np.asarray(self.locations)
+        if loc.ndim != 2 or loc.shape[1] != 3 or loc.shape[0] < 1:
+            raise ValidationError("receiver locations must have shape (n, 3), n >= 1")
+        object.__setattr__(self, "locations", np.ascontiguousarray(loc, dtype=np.int32))
+
+    @property
+    def count(self) -> int:
+        return int(self.locations.shape[0])
+
+
+@dataclass(frozen=True)
+class Sponge:
+    """Separable absorbing taper G = (gx[x]*gy[y])*gz[z] applied to the new level.
+
+    The reference keeps a zero-Dirichlet halo with no absorbing layer
+    (kernel.py:5-6); this extension multiplies the freshly updated level by G
+    before the source is injected (SURVEY.md §8(a')).  Profiles are float32
+    and equal 1 away from the faces, where the update is bit-identical to the
+    reference.
+    """
+
+    x: np.ndarray
+    y: np.ndarray
+    z: np.ndarray
+
+    def __post_init__(self):
+        for name in ("x", "y", "z"):
+            arr = np.ascontiguousarray(np.asarray(getattr(self, name), dtype=np.float32))
+            if arr.ndim != 1:
+                raise ValidationError("sponge profiles must be 1-D")
+            object.__setattr__(self, name, arr)
+
+
+@dataclass
+class KernelConfig:
+    """Mirror of fdroof.kernel.KernelConfig (kernel.py:57-101) plus extensions."""
+
+    order: int
+    dims: tuple
+    n_t: int
+    dt: float
+    h: float = 1.0
+    m: object = 1.0
+    source: Optional[Source] = None
+    receivers: Optional[Receivers] = None
+    sponge: Optional[Sponge] = None
+
+    def __post_init__(self):
+        if self.order < 2 or self.order % 2 != 0:
+            raise ValidationError(f"order must be even and >= 2, got {self.order}")
+        if self.order > 32:
+            raise ValidationError(f"order must be <= 32, got {self.order}")
+        if len(self.dims) != 3 or any(d < 1 for d in self.dims):
+            raise ValidationError(f"dims must be three positive extents, got {self.dims}")
+        if self.n_t < 0 or self.dt <= 0 or self.h <= 0:
+            raise ValidationError("n_t must be >= 0 and dt, h positive")
+        halo = self.order // 2
+        if any(d < 2 * halo + 1 for d in self.dims):
+            raise ValidationError(f"interior dims {self.dims} too small for halo width {halo}")
+        if not np.isscalar(self.m) and np.shape(self.m) != tuple(self.dims):
+            raise ValidationError("squared-slowness grid must match interior dims")
+        if self.source is not None:
+            loc = self.source.location
+            if len(loc) != 3 or any(not 0 <= c < d for c, d in zip(loc, self.dims)):
+                raise ValidationError(f"source location {loc} outside interior")
+        if self.receivers is not None:
+            loc = self.receivers.locations
+            if (loc < 0).any() or (loc >= np.asarray(self.dims)).any():
+                raise ValidationError("receiver location outside interior")
+        if self.sponge is not None:
+            if tuple(len(p) for p in (self.sponge.x, self.sponge.y, self.sponge.z)) != tuple(self.dims):
+                raise ValidationError("sponge profile lengths must match interior dims")
+        bound = max_stable_dt(self.order, self.h, self.m)
+        if self.dt > bound * (1.0 + 1e-12):
+            warnings.warn(
+                f"dt={self.dt:g} exceeds the CFL bound {bound:g}; the scheme will be unstable",
+                StabilityWarning,
+                stacklevel=2,
+            )
+
+    @property
+    def halo(self) -> int:
+        return self.order // 2
+
+    @property
+    def k(self) -> int:
+        return self.order + 1
+
+
+def row_pitch(nz: int) -> int:
+    """Device z-row pitch in floats: a multiple of 4 (16-byte rows for TMA/float4)."""
+    return (nz + 3) // 4 * 4
+
+
+class Wavefield:
+    """Three time levels in HBM, rotated by reference between steps (kernel.py:104-142).
+
+    grids[2] is the latest level u(t-1), grids[1] is u(t-2) and grids[0] the
+    scratch level that receives u(t), exactly as in the reference.  Each grid
+    is a CUDA float32 tensor of shape (nx, ny, pitch) holding the interior only
+    (z contiguous, pitch = row_pitch(nz)); the reference's zero halo is implied
+    (the kernels read zeros outside the interior), so `halo` records the
+    width a host copy is padded with.  `traces` holds receiver samples,
+    shape (rows, n_rec), when the config has receivers.
+    """
+
+    def __init__(self, halo: int, grids: list, dims: tuple, it: int = 0):
+        self.halo = int(halo)
+        self.grids = list(grids)
+        self._dims = tuple(int(d) for d in dims)
+        self.it = int(it)
+        self.traces = None
+
+    @classmethod
+    def allocate(cls, dims, halo: int, device=None) -> "Wavefield":
+        if len(dims) != 3 or any(d < 2 * halo + 1 for d in dims):
+            raise ValidationError(f"dims {tuple(dims)} too small for halo width {halo}")
+        torch = _torch()
+        _lib.load()
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        nx, ny, nz = (int(d) for d in dims)
+        shape = (nx, ny, row_pitch(nz))
+        grids = [torch.zeros(shape, dtype=torch.float32, device=dev) for _ in range(3)]
+        return cls(halo, grids, (nx, ny, nz))
+
+    @property
+    def dims(self):
+        return self._dims
+
+    @property
+    def device(self):
+        return self.grids[0].device
+
+    def interior(self, level: int = 2):
+        """Device view of a level's interior, shape dims (kernel.py:130-133)."""
+        return self.grids[level][:, :, : self._dims[2]]
+
+    def numpy(self, level: int = 2) -> np.ndarray:
+        """Host copy of a level's interior as float32, C order."""
+        return self.interior(level).cpu().numpy().copy()
+
+    def set_interior(self, level: int, values) -> None:
+        torch = _torch()
+        arr = np.ascontiguousarray(np.asarray(values, dtype=np.float32))
+        if arr.shape != self._dims:
+            raise ValidationError(f"interior values of shape {arr.shape} do not match dims {self._dims}")
+        self.interior(level).copy_(torch.from_numpy(arr))
+
+    def halo_is_zero(self) -> bool:
+        """The halo is not stored; row-padding columns must stay zero."""
+        nz = self._dims[2]
+        return all(not bool(g[:, :, nz:].any()) for g in self.grids)
+
+    def host_grids(self) -> list:
+        """The three levels as the reference lays them out: zero-padded
+        (nx+2r, ny+2r, nz+2r) float32 numpy arrays (kernel.py:119-123)."""
+        r = self.halo
+        out = []
+        for lvl in range(3):
+            padded = np.zeros(tuple(d + 2 * r for d in self._dims), dtype=np.float32)
+            padded[r : r + self._dims[0], r : r + self._dims[1], r : r + self._dims[2]] = self.numpy(lvl)
+            out.append(padded)
+        return out
+
+    @classmethod
+    def from_host_grids(cls, grids, halo: int, it: int = 0, device=None) -> "Wavefield":
+        """Upload a reference-layout Wavefield (three padded numpy levels)."""
+        r = int(halo)
+        dims = tuple(s - 2 * r for s in np.shape(grids[0]))
+        fld = cls.allocate(dims, r, device)
+        for lvl in range(3):
+            g = np.asarray(grids[lvl], dtype=np.float32)
+            fld.set_interior(lvl, g[r : r + dims[0], r : r + dims[1], r : r + dims[2]])
+        fld.it = int(it)
+        return fld
+
+
+def _check_match(fld: Wavefield, cfg: KernelConfig):
+    if fld.halo != cfg.halo or fld.dims != tuple(cfg.dims):
+        raise ValidationError(
+            f"wavefield (dims {fld.dims}, halo {fld.halo}) does not match "
+            f"config (dims {tuple(cfg.dims)}, halo {cfg.halo})"
+        )
+
+
+class _DevicePlan:
+    """Device-resident per-config constants: weights, m grid, sponge, series, receivers."""
+
+    def __init__(self, cfg: KernelConfig, device, pitch: int):
+        torch = _torch()
+        self.key = _plan_key(cfg, device)
+        self.refs = (cfg.m, cfg.source, cfg.receivers, cfg.sponge)  # keep ids alive
+        nx, ny, nz = cfg.dims
+        self.weights = acoustic_weights_f32(cfg.order)
+        self.coef = np.float32(cfg.dt * cfg.dt / (cfg.h * cfg.h))  # kernel.py:187
+        self.m_grid = None
+        self.m_scalar = np.float32(1.0)
+        if np.isscalar(cfg.m):
+            self.m_scalar = np.float32(cfg.m)  # kernel.py:189
+            self.m_mode = _lib.M_NONE if self.m_scalar == np.float32(1.0) else _lib.M_SCALAR
+        else:
+            self.m_mode = _lib.M_GRID
+            host = np.asarray(cfg.m, dtype=np.float32)  # kernel.py:188
+            self.m_grid = torch.zeros((nx, ny, pitch), dtype=torch.float32, device=device)
+            self.m_grid[:, :, :nz].copy_(torch.from_numpy(np.ascontiguousarray(host)))
+        self.sponge = None
+        if cfg.sponge is not None:
+            self.sponge = tuple(
+                torch.from_numpy(p).to(device) for p in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z)
+            )
+        self.series = None
+        self.src = (-1, 0, 0)
+        if cfg.source is not None:
+            series = np.asarray(cfg.source.series).astype(np.float32)  # kernel.py:173
+            self.series = torch.from_numpy(np.ascontiguousarray(series.reshape(-1))).to(device)
+            self.src = tuple(int(c) for c in cfg.source.location)
+        self.n_series = 0 if self.series is None else int(self.series.numel())
+        self.rec = None
+        if cfg.receivers is not None:
+            self.rec = torch.from_numpy(cfg.receivers.locations.reshape(-1).copy()).to(device)
+
+
+def _plan_key(cfg: KernelConfig, device):
+    return (cfg.order, tuple(cfg.dims), float(cfg.dt), float(cfg.h), id(cfg.m),
+            id(cfg.source), id(cfg.receivers), id(cfg.sponge), str(device))
+
+
+def _plan(cfg: KernelConfig, device, pitch: int) -> _DevicePlan:
+    plan = getattr(cfg, "_device_plan", None)
+    if plan is None or plan.key != _plan_key(cfg, device):
+        plan = _DevicePlan(cfg, device, pitch)
+        cfg._device_plan = plan
+    return plan
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _fill_args(args: _lib.AcousticArgs, cfg: KernelConfig, plan: _DevicePlan, dims, pitch_y,
+               pitch_x, it0: int, n_steps: int, variant: int):
+    args.abi_version = _lib.ABI_VERSION
+    args.order = cfg.order
+    args.nx, args.ny, args.nz = dims
+    args.pitch_y = pitch_y
+    args.pitch_x = pitch_x
+    for j, w in enumerate(plan.weights):
+        args.weights[j] = float(w)
+    args.coef = float(plan.coef)
+    args.m_mode = plan.m_mode
+    args.m_scalar = float(plan.m_scalar)
+    args.src_x, args.src_y, args.src_z = plan.src
+    args.n_series = plan.n_series
+    args.n_rec = 0 if cfg.receivers is None else cfg.receivers.count
+    args.it0 = it0
+    args.n_steps = n_steps
+    args.variant = variant
+
+
+def run(fld: Wavefield, cfg: KernelConfig, n_steps: Optional[int] = None,
+        variant: str = "auto") -> Wavefield:
+    """Advance `n_steps` (default cfg.n_t) steps in one library call.
+
+    Equivalent to calling the reference's `step` n_steps times (kernel.py:176-222):
+    levels rotate by reference, the source injects series[it] after each
+    update and `it` advances.  Work is queued on the current torch stream.
+    """
+    _check_match(fld, cfg)
+    n = cfg.n_t if n_steps is None else int(n_steps)
+    if n < 0:
+        raise ValidationError("n_steps must be >= 0")
+    if variant not in _VARIANTS:
+        raise ValidationError(f"unknown variant {variant!r}")
+    if n == 0:
+        return fld
+    torch = _torch()
+    lib = _lib.load()
+    dev = fld.device
+    for g in fld.grids:
+        if g.dtype != torch.float32 or not g.is_cuda or not g.is_contiguous() or g.shape != fld.grids[0].shape:
+            raise ValidationError("wavefield levels must be contiguous float32 CUDA tensors of one shape")
+    pitch_y = int(fld.grids[0].shape[2])
+    pitch_x = int(fld.grids[0].shape[1]) * pitch_y
+    plan = _plan(cfg, dev, pitch_y)
+    if plan.m_grid is not None and tuple(plan.m_grid.shape) != tuple(fld.grids[0].shape):
+        plan = _DevicePlan(cfg, dev, pitch_y)
+        cfg._device_plan = plan
+    args = _lib.AcousticArgs()
+    _fill_args(args, cfg, plan, fld.dims, pitch_y, pitch_x, fld.it, n, _VARIANTS[variant])
+    args.m = _ptr(plan.m_grid)
+    for i in range(3):
+        args.levels[i] = fld.grids[i].data_ptr()
+    if plan.sponge is not None:
+        args.sponge_x, args.sponge_y, args.sponge_z = (p.data_ptr() for p in plan.sponge)
+    args.series = _ptr(plan.series)
+    if plan.rec is not None:
+        rows = max(cfg.n_t, fld.it + n)
+        n_rec = cfg.receivers.count
+        if fld.traces is None or fld.traces.shape[1] != n_rec or fld.traces.shape[0] < rows:
+            grown = torch.zeros((rows, n_rec), dtype=torch.float32, device=dev)
+            if fld.traces is not None and fld.traces.shape[1] == n_rec:
+                grown[: fld.traces.shape[0]].copy_(fld.traces)
+            fld.traces = grown
+        args.rec_xyz = plan.rec.data_ptr()
+        args.traces = fld.traces.data_ptr()
+        args.trace_rows = int(fld.traces.shape[0])
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        _lib.check(lib.fdr_acoustic_run(ctypes.byref(args), ctypes.c_void_p(stream)))
+    g = fld.grids
+    fld.grids = [g[n % 3], g[(1 + n) % 3], g[(2 + n) % 3]]  # kernel.py:219, n times
+    fld.it += n
+    return fld
+
+
+def step(fld: Wavefield, cfg: KernelConfig, slabs: int = 1) -> Wavefield:
+    """Advance one time step in place; returns the same Wavefield (kernel.py:176).
+
+    `slabs` is accepted for signature compatibility: the GPU's thread-block
+    decomposition replaces the reference's x-slab threads, and results are
+    independent of it exactly as in the reference (test_kernel.py:137-144).
+    """
+    return run(fld, cfg, 1)
+
+
+@dataclass(frozen=True)
+class BenchResult:
+    """Mirror of fdroof.kernel.BenchResult (kernel.py:257-263) plus GPts/s."""
+
+    measured_gflops: float
+    point: RooflinePoint
+    wall_time_s: float
+    total_flops: float
+    wavefield: Wavefield
+
+    @property
+    def gpts_per_s(self) -> float:
+        n = float(np.prod(self.wavefield.dims))
+        steps = self.total_flops / (n * (self.point.k * 6 + 4))
+        return n * steps / self.wall_time_s / 1e9
+
+    @property
+    def achieved_gbs(self) -> float:
+        return self.gpts_per_s * ACOUSTIC_BYTES_PER_POINT
+
+
+def run_benchmark(cfg: KernelConfig, machine: Optional[MachineSpec] = None, slabs: int = 1,
+                  seed: int = 0, variant: str = "auto") -> BenchResult:
+    """Run n_t steps, time them on the device and pin the result on the roofline.
+
+    Mirrors kernel.py:266-290: the same seeded start when there is no source
+    (level 2 = standard_normal*1e-3), GFLOPS = points x kernel_flops x n_t /
+    time, with the time taken by CUDA events around the n_t launches.
+    """
+    if cfg.n_t < 1:
+        raise ValidationError("benchmark needs n_t >= 1")
+    torch = _torch()
+    fld = Wavefield.allocate(cfg.dims, cfg.halo)
+    if cfg.source is None:
+        rng = np.random.default_rng(seed)
+        fld.set_interior(2, rng.standard_normal(cfg.dims).astype(np.float32) * 1e-3)
+    _plan(cfg, fld.device, int(fld.grids[0].shape[2]))
+    stream = torch.cuda.current_stream(fld.device)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(fld.device)
+    start.record(stream)
+    run(fld, cfg, cfg.n_t, variant=variant)
+    end.record(stream)
+    end.synchronize()
+    wall = start.elapsed_time(end) / 1e3
+    n_interior = float(np.prod(cfg.dims))
+    total = n_interior * acoustic_flops_per_point(cfg.order) * cfg.n_t
+    measured = total / wall / 1e9
+    point = roofline_point(machine or b200_machine(), cfg.order, measured_gflops=measured)
+    return BenchResult(measured, point, wall, total, fld)
+
+
+def dump_wavefield(fld: Wavefield, path) -> None:
+    """Write the current level as little-endian float32, x-fastest order, with a
+    one-line `nx ny nz` sidecar at <path>.dims (kernel.py:293-301)."""
+    data = np.asarray(fld.numpy(2), dtype="<f4")
+    with open(path, "wb") as fh:
+        fh.write(data.tobytes(order="F"))
+    nx, ny, nz = fld.dims
+    with open(f"{path}.dims", "w", encoding="utf-8") as fh:
+        fh.write(f"{nx} {ny} {nz}\n")
+
+
+class HostSimulation:
+    """End-to-end simulation from host buffers through `fdr_acoustic_run_host`.
+
+    Prepares pinned host copies of the inputs, a device workspace and pinned
+    output buffers once; every `run()` then uploads m / sponge / series /
+    receivers, zeroes the levels, advances cfg.n_t steps on the GPU and
+    downloads the final interior and the traces (the whole job a user of the
+    reference's `run_benchmark` + `dump_wavefield` performs).
+    """
+
+    def __init__(self, cfg: KernelConfig, variant: str = "auto", device=None):
+        torch = _torch()
+        self.lib = _lib.load()
+        self.cfg = cfg
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        nx, ny, nz = cfg.dims
+        self.pitch_y = row_pitch(nz)
+        self.pitch_x = ny * self.pitch_y
+        self.args = _lib.AcousticArgs()
+        # host-side constants (same derivation as _DevicePlan)
+        plan = _HostPlan(cfg)
+        _fill_args(self.args, cfg, plan, cfg.dims, self.pitch_y, self.pitch_x, 0, cfg.n_t,
+                   _VARIANTS[variant])
+
+        def pinned(arr):
+            if arr is None:
+                return None
+            t = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+            return t
+
+        self.h_m = pinned(plan.m_host)
+        self.h_sponge = None if cfg.sponge is None else tuple(pinned(p) for p in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
+        self.h_series = pinned(plan.series_host)
+        self.h_rec = pinned(None if cfg.receivers is None else cfg.receivers.locations.reshape(-1))
+        self.h_final = torch.empty(tuple(cfg.dims), dtype=torch.float32).pin_memory()
+        n_rec = 0 if cfg.receivers is None else cfg.receivers.count
+        self.h_traces = torch.empty((max(cfg.n_t, 1), max(n_rec, 1)), dtype=torch.float32).pin_memory()
+        self.ws_bytes = int(self.lib.fdr_acoustic_workspace_bytes(ctypes.byref(self.args)))
+        if self.ws_bytes == 0:
+            _lib.check(_lib.FDR_EINVAL)
+        self.workspace = torch.empty(self.ws_bytes + 256, dtype=torch.uint8, device=self.device)
+        base = self.workspace.data_ptr()
+        self.ws_ptr = (base + 255) // 256 * 256
+
+    @property
+    def h2d_bytes(self) -> int:
+        tensors = [self.h_m, self.h_series, self.h_rec] + list(self.h_sponge or ())
+        return int(sum(t.numel() * t.element_size() for t in tensors if t is not None))
+
+    @property
+    def d2h_bytes(self) -> int:
+        n_rec = 0 if self.cfg.receivers is None else self.cfg.receivers.count
+        return int(self.h_final.numel() * 4 + n_rec * self.cfg.n_t * 4)
+
+    def run(self):
+        torch = _torch()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        sx, sy, sz = (None, None, None) if self.h_sponge is None else tuple(p(t) for t in self.h_sponge)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.fdr_acoustic_run_host(
+                ctypes.byref(self.args), p(self.h_m), sx, sy, sz, p(self.h_series), p(self.h_rec),
+                p(self.h_final), p(self.h_traces) if self.cfg.receivers is not None else None,
+                ctypes.c_void_p(self.ws_ptr), self.ws_bytes, ctypes.c_void_p(stream)))
+        traces = None
+        if self.cfg.receivers is not None:
+            traces = self.h_traces.numpy()[: self.cfg.n_t, : self.cfg.receivers.count]
+        return self.h_final.numpy(), traces
+
+
+class _HostPlan:
+    """Host-side float32 constants of a config (same casts as _DevicePlan)."""
+
+    def __init__(self, cfg: KernelConfig):
+        self.weights = acoustic_weights_f32(cfg.order)
+        self.coef = np.float32(cfg.dt * cfg.dt / (cfg.h * cfg.h))
+        self.m_host = None
+        self.m_scalar = np.float32(1.0)
+        if np.isscalar(cfg.m):
+            self.m_scalar = np.float32(cfg.m)
+            self.m_mode = _lib.M_NONE if self.m_scalar == np.float32(1.0) else _lib.M_SCALAR
+        else:
+            self.m_mode = _lib.M_GRID
+            self.m_host = np.ascontiguousarray(np.asarray(cfg.m, dtype=np.float32))
+        self.series_host = None
+        self.series = None
+        self.src = (-1, 0, 0)
+        if cfg.source is not None:
+            self.series_host = np.ascontiguousarray(np.asarray(cfg.source.series).astype(np.float32).reshape(-1))
+            self.series = self.series_host
+            self.src = tuple(int(c) for c in cfg.source.location)
+        self.n_series = 0 if self.series is None else int(self.series.size)
+        self.rec = None if cfg.receivers is None else cfg.receivers.locations
