@@ -12,7 +12,8 @@ import threading
 from .errors import DeviceError, ExtensionMissingError, ValidationError
 
 LIB_NAME = "libb200fd.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("B200FD_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 ABI_VERSION = 1
 MAX_RADIUS = 16
@@ -40,6 +41,8 @@ class AcousticArgs(ctypes.Structure):
         ("coef", ctypes.c_float),
         ("m_mode", _i32),
         ("m_scalar", ctypes.c_float),
+        ("m_lo", ctypes.c_float),
+        ("m_hi", ctypes.c_float),
         ("m", _vp),
         ("levels", _vp * 3),
         ("sponge_x", _vp),
@@ -75,6 +78,9 @@ EXPORTS = (
          ctypes.c_size_t, _vp),
     ),
     ("fdr_last_launch_count", ctypes.c_int64, ()),
+    ("fdr_selftest_division", ctypes.c_int64,
+     (ctypes.c_int64, ctypes.c_float, ctypes.c_float, ctypes.c_uint32,
+      ctypes.POINTER(ctypes.c_int64))),
 )
 
 _lock = threading.Lock()

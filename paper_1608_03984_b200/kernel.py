@@ -268,12 +268,14 @@ class _DevicePlan:
         self.coef = np.float32(cfg.dt * cfg.dt / (cfg.h * cfg.h))  # kernel.py:187
         self.m_grid = None
         self.m_scalar = np.float32(1.0)
+        self.m_bounds = (0.0, 0.0)
         if np.isscalar(cfg.m):
             self.m_scalar = np.float32(cfg.m)  # kernel.py:189
             self.m_mode = _lib.M_NONE if self.m_scalar == np.float32(1.0) else _lib.M_SCALAR
         else:
             self.m_mode = _lib.M_GRID
             host = np.asarray(cfg.m, dtype=np.float32)  # kernel.py:188
+            self.m_bounds = (float(host.min()), float(host.max()))
             self.m_grid = torch.zeros((nx, ny, pitch), dtype=torch.float32, device=device)
             self.m_grid[:, :, :nz].copy_(torch.from_numpy(np.ascontiguousarray(host)))
         self.sponge = None
@@ -322,6 +324,11 @@ def _fill_args(args: _lib.AcousticArgs, cfg: KernelConfig, plan: _DevicePlan, di
     args.coef = float(plan.coef)
     args.m_mode = plan.m_mode
     args.m_scalar = float(plan.m_scalar)
+    # grid bounds feed the exact division's fast-path window; NaN/inf/<=0
+    # entries make the library fall back to IEEE division everywhere
+    lo, hi = plan.m_bounds
+    ok = np.isfinite(lo) and np.isfinite(hi) and lo > 0
+    args.m_lo, args.m_hi = (lo, hi) if ok else (0.0, 0.0)
     args.src_x, args.src_y, args.src_z = plan.src
     args.n_series = plan.n_series
     args.n_rec = 0 if cfg.receivers is None else cfg.receivers.count
@@ -384,6 +391,18 @@ def run(fld: Wavefield, cfg: KernelConfig, n_steps: Optional[int] = None,
     fld.grids = [g[n % 3], g[(1 + n) % 3], g[(2 + n) % 3]]  # kernel.py:219, n times
     fld.it += n
     return fld
+
+
+def selftest_division(n: int = 1 << 26, m_lo: float = 4.9e-8, m_hi: float = 4.5e-7,
+                      seed: int = 1):
+    """Compare the kernels' branch-free division with IEEE __fdiv_rn on the
+    GPU over n hashed operand pairs; returns (mismatches, fast_path_pairs)."""
+    lib = _lib.load()
+    n_fast = ctypes.c_int64(0)
+    bad = lib.fdr_selftest_division(int(n), float(m_lo), float(m_hi), int(seed) & 0xffffffff,
+                                    ctypes.byref(n_fast))
+    _lib.check(int(bad) if bad < 0 else 0)
+    return int(bad), int(n_fast.value)
 
 
 def step(fld: Wavefield, cfg: KernelConfig, slabs: int = 1) -> Wavefield:
@@ -537,12 +556,14 @@ class _HostPlan:
         self.coef = np.float32(cfg.dt * cfg.dt / (cfg.h * cfg.h))
         self.m_host = None
         self.m_scalar = np.float32(1.0)
+        self.m_bounds = (0.0, 0.0)
         if np.isscalar(cfg.m):
             self.m_scalar = np.float32(cfg.m)
             self.m_mode = _lib.M_NONE if self.m_scalar == np.float32(1.0) else _lib.M_SCALAR
         else:
             self.m_mode = _lib.M_GRID
             self.m_host = np.ascontiguousarray(np.asarray(cfg.m, dtype=np.float32))
+            self.m_bounds = (float(self.m_host.min()), float(self.m_host.max()))
         self.series_host = None
         self.series = None
         self.src = (-1, 0, 0)
