@@ -34,7 +34,8 @@ from .roofline import (
 )
 from .stencils import abs_sum, acoustic_weights_f32, second_derivative_weights
 
-_VARIANTS = {"auto": _lib.VARIANT_AUTO, "direct": _lib.VARIANT_DIRECT, "tma": _lib.VARIANT_TMA}
+_VARIANTS = {"auto": _lib.VARIANT_AUTO, "direct": _lib.VARIANT_DIRECT, "tma": _lib.VARIANT_TMA,
+             "queue": _lib.VARIANT_QUEUE}
 
 
 def _torch():

@@ -16,6 +16,7 @@ def main():
     p.add_argument("--grid", type=int, default=512)
     p.add_argument("--nt", type=int, default=6)
     p.add_argument("--variant", default="auto")
+    p.add_argument("--random", action="store_true", help="random initial levels (no zeros)")
     a = p.parse_args()
     import torch
 
@@ -24,6 +25,12 @@ def main():
 
     cfg = config2(order=a.order, n_t=a.nt, dims=(a.grid,) * 3)
     fld = B.Wavefield.allocate(cfg.dims, cfg.halo)
+    if a.random:
+        import numpy as np
+
+        rng = np.random.default_rng(a.order)
+        fld.set_interior(2, rng.standard_normal(cfg.dims, dtype=np.float32))
+        fld.set_interior(1, rng.standard_normal(cfg.dims, dtype=np.float32))
     B.run(fld, cfg, variant=a.variant)
     torch.cuda.synchronize()
     print("ok", a.order, a.grid, a.nt, float(fld.interior().abs().max()))
