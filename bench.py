@@ -173,12 +173,15 @@ def cpu_baseline(args, cfg):
 
 
 def load_ncu_traffic(order):
+    """DRAM bytes per launch of the step kernel from the committed ncu capture
+    (profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path, encoding="utf-8") as fh:
-            return json.load(fh).get(f"order{order}")
+            entry = json.load(fh).get(f"order{order}")
     except (OSError, ValueError):
         return None
+    return None if entry is None else entry.get("traffic_bytes_per_launch")
 
 
 def main():
@@ -307,7 +310,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": traffic,
                          "peak_source": peak_src,
-                         "kernel": f"acoustic_tma<R={args.order // 2}> (one launch per time step)",
+                         "kernel": f"acoustic_queue<R={args.order // 2}> (one launch per time step)",
                          "bytes_per_launch": int(npts * 16), "launch_ms": round(launch_ms, 5)},
             "cpu_baseline": cpu,
             "e2e": e2e,
