@@ -16,7 +16,16 @@ GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built library")
-    config.addinivalue_line("markers", "slow: long-running full-size parity runs (opt-in)")
+    config.addinivalue_line("markers", "slow: long-running full-size parity runs (opt-in: FDR_SLOW=1)")
+
+
+def pytest_collection_modifyitems(config, items):
+    if os.environ.get("FDR_SLOW") == "1":
+        return
+    skip = pytest.mark.skip(reason="slow full-length parity run; set FDR_SLOW=1")
+    for item in items:
+        if "slow" in item.keywords:
+            item.add_marker(skip)
 
 
 @pytest.fixture(scope="session")
