@@ -15,6 +15,11 @@
 
 namespace fdr {
 
+// Library-wide error reporting (acoustic.cu): sets the thread-local message
+// returned by fdr_last_error() and returns `code`.
+int fail(int code, const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
 // lap + w * (a + b): one tap pair of kernel.py:205 (three roundings).
 FDR_DEV float tap(float lap, float w, float a, float b) {
   return __fadd_rn(lap, __fmul_rn(w, __fadd_rn(a, b)));
