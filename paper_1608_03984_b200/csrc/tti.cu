@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -50,6 +51,7 @@ struct TTIStep {
   int n_rec;
   float* traces;
   int gather_row;
+  int gather_pad_chunk;  // x-planes per CTA (stream kernel)
 };
 
 __device__ __forceinline__ float at(const float* u, const TTIStep& a, int x, int y, int z) {
@@ -156,10 +158,373 @@ __global__ void tti_gather_kernel(const float* p, const int* rec, int n_rec, flo
     if (e_ != cudaSuccess) return fdr::cuda_fail(e_, #call); \
   } while (0)
 
-int tti_stream_launch(const TTIStep&, const fdr_tti_args*, int, cudaStream_t, int*) {
-  return fail(FDR_EINVAL, "TTI stream kernel not built yet");
+// ============================================================ stream kernel
+// 2.5D streaming TTI step.  A CTA of 512 threads owns a 32(z) x 16(y) column
+// tile (one point per thread, a warp = one z row) and streams it along x.
+// Stream plane p (x_n = xb - R + p) arrives by TMA in one ring stage holding
+//   the p and r boxes of x_n (y/z halo: the in-plane derivatives),
+//   the in-plane Gzz coefficients cyy, czz, cyz of x_n,
+//   and, for the plane computed at this iteration (x_c = x_n - R), its
+//   k, a, b, cxx, cxy, cxz and the prev levels of p and r.
+// When x_n arrives each thread forms u, D1y u, D1z u, dyy, dzz and (through a
+// shared D1z buffer over the box rows) dyz, and the in-plane partial sums
+// gin = cyz dyz + (czz dzz + cyy dyy) and lin = dyy + dzz; x-direction values
+// travel in register windows (u, D1y u, D1z u: 2R+1 planes; gin, lin: R+1),
+// so the x derivatives dxx, dxy = D1x(D1y u), dxz = D1x(D1z u) of x_c need no
+// shared memory.  Stages are recycled by the last warp to release them (empty
+// mbarrier, as in acoustic_queue); one __syncthreads per plane orders the
+// D1z buffer.
+constexpr int TTZ = 32, TTY = 16, TNT = TTZ * TTY;
+
+template <int R>
+struct TGeo {
+  static constexpr int LZ = (R + 3) / 4 * 4;
+  static constexpr int BZ = TTZ + 2 * LZ;
+  static constexpr int BY = TTY + 2 * R;
+  static constexpr int BOX_BYTES = BZ * BY * 4;
+  static constexpr int BOX = (BOX_BYTES + 127) / 128 * 32;  // floats, 128-B aligned
+  static constexpr int TILE = TTY * TTZ;                     // 2 KB
+  static constexpr int DZ = BY * TTZ;                        // D1z rows of the box
+  // stage layout (floats)
+  static constexpr int O_BP = 0, O_BR = BOX, O_DZP = 2 * BOX, O_DZR = O_DZP + DZ;
+  static constexpr int O_IN = O_DZR + DZ;                    // cyy czz cyz (3 tiles)
+  static constexpr int O_CEN = O_IN + 3 * TILE;              // k a b cxx cxy cxz prev_p prev_r
+  static constexpr int STAGE = O_CEN + 8 * TILE;
+  static constexpr int NS = 4;
+  static constexpr int U = R <= 2 ? 2 * R + 1 : 3;           // planes per unrolled round
+  static constexpr int QW = 2 * R + U;                       // x-window length
+  static constexpr int GW = R + U;                           // delayed in-plane window
+  static constexpr int NWARPS = TNT / 32;
+  static constexpr size_t SMEM = size_t(NS) * STAGE * 4 + 2 * NS * 8;
+};
+
+struct TTIMaps {
+  CUtensorMap box_p, box_r;   // current levels, boxes with halo
+  CUtensorMap prev_p, prev_r; // previous levels, tiles
+  CUtensorMap prm[9];         // k a b cxx cyy czz cxy cyz cxz, tiles
+};
+
+FDR_DEV void mbar_arrive_t(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-int tti_stream_prepare(const fdr_tti_args*) { return FDR_OK; }
+
+FDR_DEV bool mbar_arrive_last(uint64_t* bar) {
+  uint64_t state;
+  uint32_t pending;
+  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(state) : "r"(smem_u32(bar)) : "memory");
+  asm volatile("mbarrier.pending_count.b64 %0, %1;" : "=r"(pending) : "l"(state));
+  return pending == 1;
+}
+
+template <int R>
+FDR_DEV float d1_row(const float* row, const float* w1) {  // D1 along z at row[0]
+  float d = __fmul_rn(w1[1], __fsub_rn(row[1], row[-1]));
+#pragma unroll
+  for (int j = 2; j <= R; ++j) d = __fmaf_rn(w1[j], __fsub_rn(row[j], row[-j]), d);
+  return d;
+}
+
+template <int R, bool SPONGE>
+__global__ void __launch_bounds__(TNT, 1) tti_stream(const __grid_constant__ TTIMaps maps,
+                                                     const TTIStep a) {
+  using G = TGeo<R>;
+  extern __shared__ __align__(128) float smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::NS * G::STAGE);
+  uint64_t* empty = full + G::NS;
+
+  gather(a);
+  const int tid = threadIdx.x;
+  const int tz = tid % TTZ, ty = tid / TTZ;
+  const int zt = blockIdx.x * TTZ, yt = blockIdx.y * TTY;
+  const int xb = blockIdx.z * a.gather_pad_chunk;
+  const int xe = min(a.nx, xb + a.gather_pad_chunk);
+  if (xb >= xe) return;
+  const int n = xe - xb;
+  const int nplanes = n + 2 * R;
+  const bool leader = (tid & 31) == 0;
+
+  auto issue = [&](int p, int s) {
+    float* st = smem + s * G::STAGE;
+    const int xn = xb - R + p;
+    const bool cen = p >= 2 * R;
+    const uint32_t bytes = 2 * G::BOX_BYTES + 3 * G::TILE * 4 + (cen ? 8 * G::TILE * 4 : 0);
+    mbar_arrive_expect_tx(&full[s], bytes);
+    tma_load_3d(st + G::O_BP, &maps.box_p, &full[s], zt - G::LZ, yt - R, xn);
+    tma_load_3d(st + G::O_BR, &maps.box_r, &full[s], zt - G::LZ, yt - R, xn);
+    tma_load_3d(st + G::O_IN + 0 * G::TILE, &maps.prm[4], &full[s], zt, yt, xn);  // cyy
+    tma_load_3d(st + G::O_IN + 1 * G::TILE, &maps.prm[5], &full[s], zt, yt, xn);  // czz
+    tma_load_3d(st + G::O_IN + 2 * G::TILE, &maps.prm[7], &full[s], zt, yt, xn);  // cyz
+    if (cen) {
+      const int xc = xn - R;
+      const int src[6] = {0, 1, 2, 3, 6, 8};  // k a b cxx cxy cxz
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+        tma_load_3d(st + G::O_CEN + i * G::TILE, &maps.prm[src[i]], &full[s], zt, yt, xc);
+      tma_load_3d(st + G::O_CEN + 6 * G::TILE, &maps.prev_p, &full[s], zt, yt, xc);
+      tma_load_3d(st + G::O_CEN + 7 * G::TILE, &maps.prev_r, &full[s], zt, yt, xc);
+    }
+  };
+  if (tid == 0) {
+    prefetch_tensormap(&maps.box_p);
+    prefetch_tensormap(&maps.box_r);
+    for (int s = 0; s < G::NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], G::NWARPS);
+    }
+    fence_barrier_init();
+    for (int p = 0; p < G::NS && p < nplanes; ++p) issue(p, p);
+  }
+  __syncthreads();
+
+  const int y = yt + ty, z = zt + tz;
+  const bool ok = y < a.ny && z < a.nz;
+  const int bown = (ty + R) * G::BZ + G::LZ + tz;  // own point in a box
+  const int town = ty * TTZ + tz;                   // own point in a tile
+  // halo rows of the D1z buffer this thread fills (box rows 0..R-1, TY+R..)
+  const int hrow = ty < R ? ty : (ty < 2 * R ? TTY + ty : -1);
+  float gy = 1.0f, gz = 1.0f;
+  if (SPONGE && ok) {
+    gy = a.gy[y];
+    gz = a.gz[z];
+  }
+  const bool src_here = a.sx >= 0 && y == a.sy && z == a.sz && a.it < a.n_series;
+  const float qsrc = src_here ? a.series[a.it] : 0.0f;
+  const int kinj = src_here ? a.sx - xb : -1;
+  const uint32_t px32 = (uint32_t)a.pitch_x;
+  const uint32_t oidx0 = (uint32_t)xb * px32 + (uint32_t)y * (uint32_t)a.pitch_y + (uint32_t)z;
+
+  // x-direction windows: at round base p0, index i <-> stream plane p0 - 2R + i
+  float pu[G::QW], py[G::QW], pz[G::QW], ru[G::QW], ry[G::QW], rz[G::QW];
+  // delayed in-plane sums: index i <-> stream plane p0 - R + i
+  float pg[G::GW], pl[G::GW], rg[G::GW];
+#pragma unroll
+  for (int i = 0; i < G::QW; ++i) pu[i] = py[i] = pz[i] = ru[i] = ry[i] = rz[i] = 0.0f;
+#pragma unroll
+  for (int i = 0; i < G::GW; ++i) pg[i] = pl[i] = rg[i] = 0.0f;
+
+  int slot = 0;
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (int p0 = 0; p0 < nplanes; p0 += G::U) {
+#pragma unroll
+    for (int u = 0; u < G::U; ++u) {
+      const int p = p0 + u;
+      if (p >= nplanes) break;
+      mbar_wait(&full[slot], phase);
+      float* st = smem + slot * G::STAGE;
+      // ---- in-plane work on the newest plane, both fields
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const float* box = st + (f == 0 ? G::O_BP : G::O_BR);
+        float* dzb = st + (f == 0 ? G::O_DZP : G::O_DZR);
+        const float* c0 = box + bown;
+        const float uo = c0[0];
+        float dy1 = __fmul_rn(a.w1[1], __fsub_rn(c0[G::BZ], c0[-G::BZ]));
+        float dyy = __fmul_rn(a.w2[0], uo);
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+          const float up = c0[j * G::BZ], um = c0[-j * G::BZ];
+          if (j >= 2) dy1 = __fmaf_rn(a.w1[j], __fsub_rn(up, um), dy1);
+          dyy = __fmaf_rn(a.w2[j], __fadd_rn(up, um), dyy);
+        }
+        float dz1 = __fmul_rn(a.w1[1], __fsub_rn(c0[1], c0[-1]));
+        float dzz = __fmul_rn(a.w2[0], uo);
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+          const float up = c0[j], um = c0[-j];
+          if (j >= 2) dz1 = __fmaf_rn(a.w1[j], __fsub_rn(up, um), dz1);
+          dzz = __fmaf_rn(a.w2[j], __fadd_rn(up, um), dzz);
+        }
+        dzb[(ty + R) * TTZ + tz] = dz1;
+        if (hrow >= 0) dzb[hrow * TTZ + tz] = d1_row<R>(box + hrow * G::BZ + G::LZ + tz, a.w1);
+        if (f == 0) {
+          pu[2 * R + u] = uo; py[2 * R + u] = dy1; pz[2 * R + u] = dz1;
+          pl[R + u] = __fadd_rn(dyy, dzz);
+        } else {
+          ru[2 * R + u] = uo; ry[2 * R + u] = dy1; rz[2 * R + u] = dz1;
+        }
+        // gin = fma(cyz, dyz, fma(czz, dzz, cyy dyy)): the dyz term follows the barrier
+        if (f == 0) pg[R + u] = __fmaf_rn(st[G::O_IN + 1 * G::TILE + town], dzz,
+                                          __fmul_rn(st[G::O_IN + town], dyy));
+        else rg[R + u] = __fmaf_rn(st[G::O_IN + 1 * G::TILE + town], dzz,
+                                   __fmul_rn(st[G::O_IN + town], dyy));
+      }
+      __syncthreads();  // the D1z rows of both boxes are complete
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const float* dzb = st + (f == 0 ? G::O_DZP : G::O_DZR) + (ty + R) * TTZ + tz;
+        float dyz = __fmul_rn(a.w1[1], __fsub_rn(dzb[TTZ], dzb[-TTZ]));
+#pragma unroll
+        for (int j = 2; j <= R; ++j) dyz = __fmaf_rn(a.w1[j], __fsub_rn(dzb[j * TTZ], dzb[-j * TTZ]), dyz);
+        const float cyz = st[G::O_IN + 2 * G::TILE + town];
+        if (f == 0) pg[R + u] = __fmaf_rn(cyz, dyz, pg[R + u]);
+        else rg[R + u] = __fmaf_rn(cyz, dyz, rg[R + u]);
+      }
+      // ---- the plane R behind: x derivatives and the update
+      const int k = p - 2 * R;
+      float vk = 0.f, va = 0.f, vb = 0.f, cxx = 0.f, cxy = 0.f, cxz = 0.f, ppv = 0.f, rpv = 0.f;
+      if (k >= 0) {
+        const float* cen = st + G::O_CEN + town;
+        vk = cen[0]; va = cen[G::TILE]; vb = cen[2 * G::TILE];
+        cxx = cen[3 * G::TILE]; cxy = cen[4 * G::TILE]; cxz = cen[5 * G::TILE];
+        ppv = cen[6 * G::TILE]; rpv = cen[7 * G::TILE];
+      }
+      // release the stage (every read of it is above)
+      __syncwarp();
+      if (leader && mbar_arrive_last(&empty[slot])) {
+        mbar_wait(&empty[slot], phase);
+        if (p + G::NS < nplanes) issue(p + G::NS, slot);
+      }
+      if (++slot == G::NS) {
+        slot = 0;
+        phase ^= 1u;
+      }
+      if (k >= 0) {
+        // window index of the centre plane (stream plane p - R): u + R
+        float Gf[2], Lp = 0.f;
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          const float* qu = f == 0 ? pu : ru;
+          const float* qy = f == 0 ? py : ry;
+          const float* qz = f == 0 ? pz : rz;
+          const int c = u + R;
+          float dxx = __fmul_rn(a.w2[0], qu[c]);
+          float dxy = __fmul_rn(a.w1[1], __fsub_rn(qy[c + 1], qy[c - 1]));
+          float dxz = __fmul_rn(a.w1[1], __fsub_rn(qz[c + 1], qz[c - 1]));
+#pragma unroll
+          for (int j = 1; j <= R; ++j) {
+            dxx = __fmaf_rn(a.w2[j], __fadd_rn(qu[c + j], qu[c - j]), dxx);
+            if (j >= 2) {
+              dxy = __fmaf_rn(a.w1[j], __fsub_rn(qy[c + j], qy[c - j]), dxy);
+              dxz = __fmaf_rn(a.w1[j], __fsub_rn(qz[c + j], qz[c - j]), dxz);
+            }
+          }
+          const float gin = f == 0 ? pg[u] : rg[u];
+          Gf[f] = __fmaf_rn(cxz, dxz, __fmaf_rn(cxy, dxy, __fmaf_rn(cxx, dxx, gin)));
+          if (f == 0) Lp = __fadd_rn(pl[u], dxx);
+        }
+        const float Hp = __fsub_rn(Lp, Gf[0]);
+        const float pc = pu[u + R], rc = ru[u + R];
+        float pn = __fmaf_rn(vk, __fmaf_rn(va, Hp, __fmul_rn(vb, Gf[1])), __fmaf_rn(2.0f, pc, -ppv));
+        float rn = __fmaf_rn(vk, __fmaf_rn(vb, Hp, Gf[1]), __fmaf_rn(2.0f, rc, -rpv));
+        if (SPONGE) {
+          const float g = __fmul_rn(__fmul_rn(__ldg(a.gx + xb + k), gy), gz);
+          pn = __fmul_rn(pn, g);
+          rn = __fmul_rn(rn, g);
+        }
+        if (k == kinj) {
+          pn = __fadd_rn(pn, qsrc);
+          rn = __fadd_rn(rn, qsrc);
+        }
+        if (ok) {
+          const uint32_t o = oidx0 + (uint32_t)k * px32;
+          a.pn[o] = pn;
+          a.rn[o] = rn;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2 * R; ++i) {
+      pu[i] = pu[i + G::U]; py[i] = py[i + G::U]; pz[i] = pz[i + G::U];
+      ru[i] = ru[i + G::U]; ry[i] = ry[i + G::U]; rz[i] = rz[i + G::U];
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      pg[i] = pg[i + G::U]; pl[i] = pl[i + G::U]; rg[i] = rg[i + G::U];
+    }
+  }
+}
+
+static int tti_encode(CUtensorMap* map, const float* base, const fdr_tti_args* a, int bz, int by) {
+  typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                          CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                          CUtensorMapFloatOOBfill);
+  static Enc enc = nullptr;
+  if (!enc) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(FDR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = reinterpret_cast<Enc>(p);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)a->nz, (cuuint64_t)a->ny, (cuuint64_t)a->nx};
+  cuuint64_t strides[2] = {(cuuint64_t)a->pitch_y * 4, (cuuint64_t)a->pitch_x * 4};
+  cuuint32_t box[3] = {(cuuint32_t)bz, (cuuint32_t)by, 1}, es[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FDR_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return FDR_OK;
+}
+
+template <int R>
+static int stream_inst(const TTIStep& s, const fdr_tti_args* a, int k, cudaStream_t st,
+                       int* chunk_cache) {
+  using G = TGeo<R>;
+  const bool sponge = s.gx != nullptr;
+  auto kern = sponge ? tti_stream<R, true> : tti_stream<R, false>;
+  static int configured[2] = {-1, -1};
+  static int occ = 1, nsm = 148;
+  int dev = 0;
+  TTI_CUDA(cudaGetDevice(&dev));
+  if (configured[sponge] != dev) {
+    TTI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    TTI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TNT, G::SMEM));
+    TTI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (occ < 1) return fail(FDR_ECUDA, "TTI stream kernel (r=%d) cannot be resident", R);
+    configured[sponge] = dev;
+  }
+  TTIMaps maps;
+  const int cur = (2 + k) % 3, prev = (1 + k) % 3;
+  int rc = tti_encode(&maps.box_p, a->p[cur], a, G::BZ, G::BY);
+  if (rc == FDR_OK) rc = tti_encode(&maps.box_r, a->r[cur], a, G::BZ, G::BY);
+  if (rc == FDR_OK) rc = tti_encode(&maps.prev_p, a->p[prev], a, TTZ, TTY);
+  if (rc == FDR_OK) rc = tti_encode(&maps.prev_r, a->r[prev], a, TTZ, TTY);
+  for (int i = 0; i < 9 && rc == FDR_OK; ++i) rc = tti_encode(&maps.prm[i], a->params[i], a, TTZ, TTY);
+  if (rc != FDR_OK) return rc;
+  TTIStep t = s;
+  const int tzn = (a->nz + TTZ - 1) / TTZ, tyn = (a->ny + TTY - 1) / TTY;
+  if (*chunk_cache <= 0) {
+    const long tiles = (long)tzn * tyn, slots = (long)occ * nsm;
+    double best = 1e30;
+    int best_c = 1;
+    for (int c = 1; c <= std::max(1, a->nx / (2 * R)); ++c) {
+      const int len = (a->nx + c - 1) / c;
+      const int cc = (a->nx + len - 1) / len;
+      const long waves = (tiles * cc + slots - 1) / slots;
+      const double tt = (double)waves * (len + 0.3 * 2 * R);
+      if (tt < best * 0.999) {
+        best = tt;
+        best_c = cc;
+      }
+    }
+    *chunk_cache = (a->nx + best_c - 1) / best_c;
+  }
+  t.gather_pad_chunk = *chunk_cache;
+  dim3 grid(tzn, tyn, (a->nx + t.gather_pad_chunk - 1) / t.gather_pad_chunk);
+  kern<<<grid, TNT, G::SMEM, st>>>(maps, t);
+  TTI_CUDA(cudaGetLastError());
+  return FDR_OK;
+}
+
+int tti_stream_launch(const TTIStep& s, const fdr_tti_args* a, int k, cudaStream_t st,
+                      int* chunk_cache) {
+  switch (a->order / 2) {
+    case 1: return stream_inst<1>(s, a, k, st, chunk_cache);
+    case 2: return stream_inst<2>(s, a, k, st, chunk_cache);
+    case 3: return stream_inst<3>(s, a, k, st, chunk_cache);
+    case 4: return stream_inst<4>(s, a, k, st, chunk_cache);
+    default: return fail(FDR_EINVAL, "TTI stream kernel supports orders 2..8, got %d", a->order);
+  }
+}
+
+int tti_stream_prepare(const fdr_tti_args* a) {
+  if ((uint64_t)a->nx * (uint64_t)a->pitch_x >= (1ull << 32))
+    return fail(FDR_EINVAL, "the TTI stream kernel indexes grids of < 2^32 elements");
+  return FDR_OK;
+}
 
 static int validate(const fdr_tti_args* a) {
   if (!a) return fail(FDR_EINVAL, "args is NULL");
@@ -227,7 +592,10 @@ void fill(TTIStep& s, const fdr_tti_args* a, int k) {
 }
 
 static int run(const fdr_tti_args* a, cudaStream_t st) {
-  int variant = a->variant == FDR_VARIANT_AUTO ? FDR_VARIANT_DIRECT : a->variant;
+  int variant = a->variant;
+  if (variant == FDR_VARIANT_AUTO)
+    variant = (a->order <= 8 && (uint64_t)a->nx * (uint64_t)a->pitch_x < (1ull << 32))
+                  ? FDR_VARIANT_QUEUE : FDR_VARIANT_DIRECT;
   if (variant == FDR_VARIANT_QUEUE && a->n_steps > 0) {
     int rc = tti_stream_prepare(a);
     if (rc != FDR_OK) return rc;

@@ -118,7 +118,7 @@ def _gpu(tti_mod, cfg, variant, n=None):
     return fld
 
 
-GPU_VARIANTS = ["direct"]
+GPU_VARIANTS = ["stream", "direct"]
 
 
 @pytest.mark.gpu
@@ -133,4 +133,25 @@ def test_gpu_tti_bitexact_vs_c_oracle(tti_mod, variant, order, dims):
     assert sha(fld.numpy("p")) == sha(st.interior("p"))
     assert sha(fld.numpy("r")) == sha(st.interior("r"))
     assert sha(fld.numpy("p", 1)) == sha(st.interior("p", 1))
+    assert (fld.traces.cpu().numpy() == st.traces).all()
+
+
+@pytest.mark.gpu
+def test_gpu_tti_config4_grid_vs_c_oracle(tti_mod):
+    """BASELINE config 4 (384^3, order 8, smooth eps/delta/tilt/azimuth,
+    sponge, source, receivers) for 3 steps from random levels, bit-exact."""
+    cfg = tti_mod.config4(n_t=3)
+    rng = np.random.default_rng(4)
+    st = T.TTIState(cfg.dims, cfg.halo)
+    fld = tti_mod.TTIWavefield.allocate(cfg.dims, cfg.halo)
+    for f in ("p", "r"):
+        for lvl in (1, 2):
+            v = rng.standard_normal(cfg.dims, dtype=np.float32)
+            st.interior(f, lvl)[...] = v
+            fld.set_interior(f, lvl, v)
+    tti_mod.tti_run(fld, cfg)
+    w2, w1 = tti_weights_f32(8)
+    T.simulate_c(cfg, cfg.params(), w2, w1, state=st)
+    assert sha(fld.numpy("p")) == sha(st.interior("p"))
+    assert sha(fld.numpy("r")) == sha(st.interior("r"))
     assert (fld.traces.cpu().numpy() == st.traces).all()
