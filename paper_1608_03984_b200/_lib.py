@@ -80,6 +80,8 @@ EXPORTS = (
     ("fdr_last_launch_count", ctypes.c_int64, ()),
     ("fdr_tti_args_size", ctypes.c_size_t, ()),
     ("fdr_tti_run", ctypes.c_int, (ctypes.c_void_p, _vp)),
+    ("fdr_elastic_args_size", ctypes.c_size_t, ()),
+    ("fdr_elastic_run", ctypes.c_int, (ctypes.c_void_p, _vp)),
     ("fdr_selftest_division", ctypes.c_int64,
      (ctypes.c_int64, ctypes.c_float, ctypes.c_float, ctypes.c_uint32,
       ctypes.POINTER(ctypes.c_int64))),
