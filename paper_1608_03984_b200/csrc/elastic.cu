@@ -90,7 +90,6 @@ __device__ __forceinline__ float taper(const ElStep& a, int x, int y, int z) {
 
 // velocity pass, one thread per point (checker variant)
 __global__ void __launch_bounds__(256) el_vel_direct(const ElStep a) {
-  gather_vz(a);
   const int z = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   const int x = blockIdx.z;
@@ -118,6 +117,7 @@ __global__ void __launch_bounds__(256) el_vel_direct(const ElStep a) {
 
 // stress pass, one thread per point (checker variant)
 __global__ void __launch_bounds__(256) el_str_direct(const ElStep a) {
+  gather_vz(a);  // vz is final for this step and not written by the stress pass
   const int z = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   const int x = blockIdx.z;
@@ -147,15 +147,6 @@ __global__ void __launch_bounds__(256) el_str_direct(const ElStep a) {
   }
 #pragma unroll
   for (int i = 0; i < 6; ++i) a.f[SXX + i][o] = s[i];
-}
-
-__global__ void el_gather_kernel(const float* vz, const int* rec, int n_rec, float* traces, int row,
-                                 int pitch_y, long long pitch_x) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n_rec) {
-    const int* q = rec + 3 * i;
-    traces[(size_t)row * n_rec + i] = vz[(size_t)q[0] * pitch_x + (size_t)q[1] * pitch_y + q[2]];
-  }
 }
 
 #define EL_CUDA(call)                                        \
@@ -221,8 +212,9 @@ static void fill(ElStep& s, const fdr_elastic_args* a, int k) {
   s.rec = a->rec_xyz;
   s.n_rec = a->n_rec;
   s.traces = a->traces;
-  const int row = s.it - 1;
-  s.gather_row = (k > 0 && a->n_rec > 0 && a->traces && row < a->trace_rows) ? row : -1;
+  // receivers sample vz at the start of the stress pass (vz is final for
+  // step `it` there and the stress pass does not write it)
+  s.gather_row = (a->n_rec > 0 && a->traces && s.it < a->trace_rows) ? s.it : -1;
 }
 
 static int run(const fdr_elastic_args* a, cudaStream_t st) {
@@ -247,17 +239,374 @@ static int run(const fdr_elastic_args* a, cudaStream_t st) {
       EL_CUDA(cudaGetLastError());
     }
   }
-  const int last = a->it0 + a->n_steps - 1;
-  if (a->n_steps > 0 && a->n_rec > 0 && a->traces && last < a->trace_rows) {
-    el_gather_kernel<<<(a->n_rec + 255) / 256, 256, 0, st>>>(a->fields[VZ], a->rec_xyz, a->n_rec,
-                                                             a->traces, last, a->pitch_y, a->pitch_x);
-    EL_CUDA(cudaGetLastError());
-  }
   return FDR_OK;
 }
 
-int el_stream_step(const ElStep&, const fdr_elastic_args*, cudaStream_t, int*) {
-  return fail(FDR_EINVAL, "elastic stream kernel not built yet");
+// ============================================================ stream kernels
+// 2.5D streaming velocity and stress passes.  A CTA of 512 threads owns a
+// 32(z) x 16(y) column tile (one point per thread) and streams it along x.
+// Stream plane p (x_n = xb - R + p) arrives by TMA in one ring stage with the
+// boxes (y/z halo) of the fields whose y/z derivatives the pass needs, and the
+// halo-free tiles of the plane computed at this iteration (x_c = x_n - R):
+// the fields it updates in place and its parameters.  In-plane derivative
+// sums are formed on arrival and delayed R planes in registers; the x
+// derivatives read register windows of own-column values.  Stages are
+// recycled by the last warp to release them (empty mbarrier).
+constexpr int ETZ = 32, ETY = 16, ENT = ETZ * ETY;
+
+template <int R, int NBOX, int NTILE>
+struct EGeo {
+  static constexpr int LZ = (R + 3) / 4 * 4;
+  static constexpr int BZ = ETZ + 2 * LZ;
+  static constexpr int BY = ETY + 2 * R;
+  static constexpr int BOX_BYTES = BZ * BY * 4;
+  static constexpr int BOX = (BOX_BYTES + 127) / 128 * 32;
+  static constexpr int TILE = ETY * ETZ;
+  static constexpr int O_TILE = NBOX * BOX;
+  static constexpr int STAGE = O_TILE + NTILE * TILE;
+  static constexpr int NS = 4;
+  static constexpr int U = R <= 2 ? 2 * R + 1 : 3;
+  static constexpr int QW = 2 * R + U;
+  static constexpr int GW = R + U;
+  static constexpr int NWARPS = ENT / 32;
+  static constexpr size_t SMEM = size_t(NS) * STAGE * 4 + 2 * NS * 8;
+};
+
+struct ElMaps {
+  CUtensorMap box[5];   // velocity pass: sxy sxz syy syz szz; stress pass: vx vy vz
+  CUtensorMap tile[9];  // velocity pass: sxx vx vy vz bs; stress: sxx..syz lam mu
+};
+
+FDR_DEV bool el_arrive_last(uint64_t* bar) {
+  uint64_t state;
+  uint32_t pending;
+  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(state) : "r"(smem_u32(bar)) : "memory");
+  asm volatile("mbarrier.pending_count.b64 %0, %1;" : "=r"(pending) : "l"(state));
+  return pending == 1;
+}
+
+// staggered differences on a strided line (p points at the own element)
+template <int R>
+FDR_DEV float sF(const float* p, int s, const float* c) {
+  float d = __fmul_rn(c[1], __fsub_rn(p[s], p[0]));
+#pragma unroll
+  for (int k = 2; k <= R; ++k) d = __fmaf_rn(c[k], __fsub_rn(p[k * s], p[(1 - k) * s]), d);
+  return d;
+}
+template <int R>
+FDR_DEV float sB(const float* p, int s, const float* c) {
+  float d = __fmul_rn(c[1], __fsub_rn(p[0], p[-s]));
+#pragma unroll
+  for (int k = 2; k <= R; ++k) d = __fmaf_rn(c[k], __fsub_rn(p[(k - 1) * s], p[-k * s]), d);
+  return d;
+}
+// the same on a register window w (centre index c)
+template <int R>
+FDR_DEV float wF(const float* w, int c, const float* cc) {
+  float d = __fmul_rn(cc[1], __fsub_rn(w[c + 1], w[c]));
+#pragma unroll
+  for (int k = 2; k <= R; ++k) d = __fmaf_rn(cc[k], __fsub_rn(w[c + k], w[c + 1 - k]), d);
+  return d;
+}
+template <int R>
+FDR_DEV float wB(const float* w, int c, const float* cc) {
+  float d = __fmul_rn(cc[1], __fsub_rn(w[c], w[c - 1]));
+#pragma unroll
+  for (int k = 2; k <= R; ++k) d = __fmaf_rn(cc[k], __fsub_rn(w[c + k - 1], w[c - k]), d);
+  return d;
+}
+
+// PASS 0: velocity (boxes sxy sxz syy syz szz; tiles sxx [newest], vx vy vz bs [centre])
+// PASS 1: stress   (boxes vx vy vz;            tiles sxx syy szz sxy sxz syz lam mu [centre])
+template <int R, int PASS, bool SPONGE>
+__global__ void __launch_bounds__(ENT, 1) el_stream(const __grid_constant__ ElMaps maps,
+                                                    const ElStep a) {
+  constexpr int NBOX = PASS == 0 ? 5 : 3;
+  constexpr int NTILE = PASS == 0 ? 5 : 8;
+  using G = EGeo<R, NBOX, NTILE>;
+  extern __shared__ __align__(128) float smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::NS * G::STAGE);
+  uint64_t* empty = full + G::NS;
+
+  if (PASS == 1) gather_vz(a);
+  const int tid = threadIdx.x;
+  const int tz = tid % ETZ, ty = tid / ETZ;
+  const int zt = blockIdx.x * ETZ, yt = blockIdx.y * ETY;
+  const int xb = blockIdx.z * a.chunk;
+  const int xe = min(a.nx, xb + a.chunk);
+  if (xb >= xe) return;
+  const int n = xe - xb;
+  const int nplanes = n + 2 * R;
+  const bool leader = (tid & 31) == 0;
+
+  auto issue = [&](int pl, int s) {
+    float* st = smem + s * G::STAGE;
+    const int xn = xb - R + pl;
+    const bool cen = pl >= 2 * R;
+    const int ncen = PASS == 0 ? 4 : 8;  // centre tiles
+    const uint32_t bytes = NBOX * G::BOX_BYTES + (PASS == 0 ? G::TILE * 4 : 0) +
+                           (cen ? ncen * G::TILE * 4 : 0);
+    mbar_arrive_expect_tx(&full[s], bytes);
+#pragma unroll
+    for (int b = 0; b < NBOX; ++b)
+      tma_load_3d(st + b * G::BOX, &maps.box[b], &full[s], zt - G::LZ, yt - R, xn);
+    if (PASS == 0) tma_load_3d(st + G::O_TILE, &maps.tile[0], &full[s], zt, yt, xn);
+    if (cen) {
+      const int t0 = PASS == 0 ? 1 : 0;
+#pragma unroll
+      for (int t = 0; t < (PASS == 0 ? 4 : 8); ++t)
+        tma_load_3d(st + G::O_TILE + (t0 + t) * G::TILE, &maps.tile[t0 + t], &full[s], zt, yt,
+                    xn - R);
+    }
+  };
+  if (tid == 0) {
+    for (int b = 0; b < NBOX; ++b) prefetch_tensormap(&maps.box[b]);
+    for (int s = 0; s < G::NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], G::NWARPS);
+    }
+    fence_barrier_init();
+    for (int pl = 0; pl < G::NS && pl < nplanes; ++pl) issue(pl, pl);
+  }
+  __syncthreads();
+
+  const int y = yt + ty, z = zt + tz;
+  const bool ok = y < a.ny && z < a.nz;
+  const int bown = (ty + R) * G::BZ + G::LZ + tz;
+  const int town = ty * ETZ + tz;
+  float gyz = 1.0f, gy = 1.0f, gz = 1.0f;
+  if (SPONGE && ok) {
+    gy = a.gy[y];
+    gz = a.gz[z];
+  }
+  (void)gyz;
+  const bool src_here = PASS == 1 && a.sx >= 0 && y == a.sy && z == a.sz && a.it < a.n_series;
+  const float qsrc = src_here ? a.series[a.it] : 0.0f;
+  const int kinj = src_here ? a.sx - xb : -1;
+  const uint32_t px32 = (uint32_t)a.pitch_x;
+  const uint32_t oidx0 = (uint32_t)xb * px32 + (uint32_t)y * (uint32_t)a.pitch_y + (uint32_t)z;
+
+  // x windows (index i <-> stream plane p0 - 2R + i) and delayed in-plane
+  // values (index i <-> stream plane p0 - R + i)
+  float w0[G::QW], w1[G::QW], w2[G::QW];
+  constexpr int ND = PASS == 0 ? 3 : 5;
+  float dly[ND][G::GW];
+#pragma unroll
+  for (int i = 0; i < G::QW; ++i) w0[i] = w1[i] = w2[i] = 0.0f;
+#pragma unroll
+  for (int d = 0; d < ND; ++d)
+#pragma unroll
+    for (int i = 0; i < G::GW; ++i) dly[d][i] = 0.0f;
+
+  int slot = 0;
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (int p0 = 0; p0 < nplanes; p0 += G::U) {
+#pragma unroll
+    for (int u = 0; u < G::U; ++u) {
+      const int pl = p0 + u;
+      if (pl >= nplanes) break;
+      mbar_wait(&full[slot], phase);
+      const float* st = smem + slot * G::STAGE;
+      const int qn = 2 * R + u, gn = R + u;
+      if (PASS == 0) {
+        const float* sxy = st + 0 * G::BOX + bown;
+        const float* sxz = st + 1 * G::BOX + bown;
+        const float* syy = st + 2 * G::BOX + bown;
+        const float* syz = st + 3 * G::BOX + bown;
+        const float* szz = st + 4 * G::BOX + bown;
+        w0[qn] = st[G::O_TILE + town];  // sxx
+        w1[qn] = sxy[0];
+        w2[qn] = sxz[0];
+        dly[0][gn] = __fadd_rn(sB<R>(sxy, G::BZ, a.c), sB<R>(sxz, 1, a.c));
+        dly[1][gn] = __fadd_rn(sF<R>(syy, G::BZ, a.c), sB<R>(syz, 1, a.c));
+        dly[2][gn] = __fadd_rn(sB<R>(syz, G::BZ, a.c), sF<R>(szz, 1, a.c));
+      } else {
+        const float* vx = st + 0 * G::BOX + bown;
+        const float* vy = st + 1 * G::BOX + bown;
+        const float* vz = st + 2 * G::BOX + bown;
+        w0[qn] = vx[0];
+        w1[qn] = vy[0];
+        w2[qn] = vz[0];
+        dly[0][gn] = sB<R>(vy, G::BZ, a.c);                            // ey
+        dly[1][gn] = sB<R>(vz, 1, a.c);                                // ez
+        dly[2][gn] = sF<R>(vx, G::BZ, a.c);                            // Fy vx
+        dly[3][gn] = sF<R>(vx, 1, a.c);                                // Fz vx
+        dly[4][gn] = __fadd_rn(sF<R>(vy, 1, a.c), sF<R>(vz, G::BZ, a.c));  // Fz vy + Fy vz
+      }
+      const int k = pl - 2 * R;
+      float cen[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) cen[t] = 0.0f;
+      if (k >= 0) {
+        const float* ct = st + G::O_TILE + (PASS == 0 ? G::TILE : 0) + town;
+#pragma unroll
+        for (int t = 0; t < (PASS == 0 ? 4 : 8); ++t) cen[t] = ct[t * G::TILE];
+      }
+      __syncwarp();
+      if (leader && el_arrive_last(&empty[slot])) {
+        mbar_wait(&empty[slot], phase);
+        if (pl + G::NS < nplanes) issue(pl + G::NS, slot);
+      }
+      if (++slot == G::NS) {
+        slot = 0;
+        phase ^= 1u;
+      }
+      if (k >= 0) {
+        const int c = u + R;
+        const uint32_t o = oidx0 + (uint32_t)k * px32;
+        const float g = SPONGE ? __fmul_rn(__fmul_rn(__ldg(a.gx + xb + k), gy), gz) : 1.0f;
+        if (PASS == 0) {
+          const float b = cen[3];
+          float vx = __fmaf_rn(b, __fadd_rn(dly[0][u], wF<R>(w0, c, a.c)), cen[0]);
+          float vy = __fmaf_rn(b, __fadd_rn(dly[1][u], wB<R>(w1, c, a.c)), cen[1]);
+          float vz = __fmaf_rn(b, __fadd_rn(dly[2][u], wB<R>(w2, c, a.c)), cen[2]);
+          if (SPONGE) {
+            vx = __fmul_rn(vx, g);
+            vy = __fmul_rn(vy, g);
+            vz = __fmul_rn(vz, g);
+          }
+          if (ok) {
+            a.f[VX][o] = vx;
+            a.f[VY][o] = vy;
+            a.f[VZ][o] = vz;
+          }
+        } else {
+          const float lam = cen[6], mu = cen[7];
+          const float l2m = __fmaf_rn(2.0f, mu, lam);
+          const float ex = wB<R>(w0, c, a.c);
+          const float ey = dly[0][u], ez = dly[1][u];
+          float sv[6];
+          sv[0] = __fmaf_rn(lam, __fadd_rn(ey, ez), __fmaf_rn(l2m, ex, cen[0]));
+          sv[1] = __fmaf_rn(lam, __fadd_rn(ez, ex), __fmaf_rn(l2m, ey, cen[1]));
+          sv[2] = __fmaf_rn(lam, __fadd_rn(ey, ex), __fmaf_rn(l2m, ez, cen[2]));
+          sv[3] = __fmaf_rn(mu, __fadd_rn(dly[2][u], wF<R>(w1, c, a.c)), cen[3]);
+          sv[4] = __fmaf_rn(mu, __fadd_rn(dly[3][u], wF<R>(w2, c, a.c)), cen[4]);
+          sv[5] = __fmaf_rn(mu, dly[4][u], cen[5]);
+          if (SPONGE) {
+#pragma unroll
+            for (int i = 0; i < 6; ++i) sv[i] = __fmul_rn(sv[i], g);
+          }
+          if (k == kinj) {
+            sv[0] = __fadd_rn(sv[0], qsrc);
+            sv[1] = __fadd_rn(sv[1], qsrc);
+            sv[2] = __fadd_rn(sv[2], qsrc);
+          }
+          if (ok) {
+#pragma unroll
+            for (int i = 0; i < 6; ++i) a.f[SXX + i][o] = sv[i];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2 * R; ++i) {
+      w0[i] = w0[i + G::U];
+      w1[i] = w1[i + G::U];
+      w2[i] = w2[i + G::U];
+    }
+#pragma unroll
+    for (int d = 0; d < ND; ++d)
+#pragma unroll
+      for (int i = 0; i < R; ++i) dly[d][i] = dly[d][i + G::U];
+  }
+}
+
+static int el_encode(CUtensorMap* map, const float* base, const fdr_elastic_args* a, int bz, int by) {
+  typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                          CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                          CUtensorMapFloatOOBfill);
+  static Enc enc = nullptr;
+  if (!enc) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(FDR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = reinterpret_cast<Enc>(p);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)a->nz, (cuuint64_t)a->ny, (cuuint64_t)a->nx};
+  cuuint64_t strides[2] = {(cuuint64_t)a->pitch_y * 4, (cuuint64_t)a->pitch_x * 4};
+  cuuint32_t box[3] = {(cuuint32_t)bz, (cuuint32_t)by, 1}, es[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FDR_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return FDR_OK;
+}
+
+template <int R, int PASS>
+static int el_launch(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, int chunk) {
+  constexpr int NBOX = PASS == 0 ? 5 : 3;
+  constexpr int NTILE = PASS == 0 ? 5 : 8;
+  using G = EGeo<R, NBOX, NTILE>;
+  const bool sponge = s.gx != nullptr;
+  auto kern = sponge ? el_stream<R, PASS, true> : el_stream<R, PASS, false>;
+  static int configured[2] = {-1, -1};
+  int dev = 0;
+  EL_CUDA(cudaGetDevice(&dev));
+  if (configured[sponge] != dev) {
+    EL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    configured[sponge] = dev;
+  }
+  ElMaps maps;
+  const int boxes0[5] = {SXY, SXZ, SYY, SYZ, SZZ}, boxes1[3] = {VX, VY, VZ};
+  int rc = FDR_OK;
+  for (int b = 0; b < NBOX && rc == FDR_OK; ++b)
+    rc = el_encode(&maps.box[b], a->fields[PASS == 0 ? boxes0[b] : boxes1[b]], a, G::BZ, G::BY);
+  if (PASS == 0) {
+    const float* t[5] = {a->fields[SXX], a->fields[VX], a->fields[VY], a->fields[VZ], a->params[0]};
+    for (int i = 0; i < 5 && rc == FDR_OK; ++i) rc = el_encode(&maps.tile[i], t[i], a, ETZ, ETY);
+  } else {
+    const float* t[8] = {a->fields[SXX], a->fields[SYY], a->fields[SZZ], a->fields[SXY],
+                         a->fields[SXZ], a->fields[SYZ], a->params[1], a->params[2]};
+    for (int i = 0; i < 8 && rc == FDR_OK; ++i) rc = el_encode(&maps.tile[i], t[i], a, ETZ, ETY);
+  }
+  if (rc != FDR_OK) return rc;
+  ElStep t = s;
+  t.chunk = chunk;
+  dim3 grid((a->nz + ETZ - 1) / ETZ, (a->ny + ETY - 1) / ETY, (a->nx + chunk - 1) / chunk);
+  kern<<<grid, ENT, G::SMEM, st>>>(maps, t);
+  EL_CUDA(cudaGetLastError());
+  return FDR_OK;
+}
+
+template <int R>
+static int el_step_r(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, int* chunk_cache) {
+  if (*chunk_cache <= 0) {
+    int nsm = 148;
+    int dev = 0;
+    EL_CUDA(cudaGetDevice(&dev));
+    EL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const long tiles = (long)((a->nz + ETZ - 1) / ETZ) * ((a->ny + ETY - 1) / ETY), slots = nsm;
+    double best = 1e30;
+    int best_c = 1;
+    for (int c = 1; c <= std::max(1, a->nx / (2 * R)); ++c) {
+      const int len = (a->nx + c - 1) / c;
+      const int cc = (a->nx + len - 1) / len;
+      const long waves = (tiles * cc + slots - 1) / slots;
+      const double tt = (double)waves * (len + 0.3 * 2 * R);
+      if (tt < best * 0.999) {
+        best = tt;
+        best_c = cc;
+      }
+    }
+    *chunk_cache = (a->nx + best_c - 1) / best_c;
+  }
+  int rc = el_launch<R, 0>(s, a, st, *chunk_cache);
+  if (rc == FDR_OK) rc = el_launch<R, 1>(s, a, st, *chunk_cache);
+  return rc;
+}
+
+int el_stream_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, int* chunk_cache) {
+  switch (a->order / 2) {
+    case 1: return el_step_r<1>(s, a, st, chunk_cache);
+    case 2: return el_step_r<2>(s, a, st, chunk_cache);
+    case 3: return el_step_r<3>(s, a, st, chunk_cache);
+    case 4: return el_step_r<4>(s, a, st, chunk_cache);
+    default: return fail(FDR_EINVAL, "elastic stream kernel supports orders 2..8, got %d", a->order);
+  }
 }
 
 }  // namespace fdr_el

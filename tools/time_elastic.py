@@ -1,0 +1,36 @@
+"""Time the elastic velocity-stress step on BASELINE config 5 (320^3, order 8)."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import numpy as np
+    import torch
+
+    from paper_1608_03984_b200 import elastic
+
+    nt = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+    cfg = elastic.config5(n_t=nt)
+    npts = float(np.prod(cfg.dims))
+    for variant in ("stream",):
+        fld = elastic.ElasticWavefield.allocate(cfg.dims, cfg.halo)
+        elastic.elastic_run(fld, cfg, 2, variant=variant)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        elastic.elastic_run(fld, cfg, nt, variant=variant)
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e) / nt
+        g = npts / ms / 1e6
+        print(json.dumps({"variant": variant, "ms_per_step": round(ms, 4), "gpts": round(g, 2),
+                          "gbs_84B": round(g * 84, 1), "gbs_120B_two_pass": round(g * 120, 1)}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
