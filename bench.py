@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--no-configs", action="store_true",
+                   help="skip the BASELINE configs 1, 3, 4, 5 lines")
     return p.parse_args()
 
 
@@ -170,6 +172,81 @@ def cpu_baseline(args, cfg):
     return {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"{args.cpu_steps} time steps of the {cfg.dims[0]}^3 order-{cfg.order} "
                       "update (numpy port of fdroof.kernel.step, x-slab threads)"}
+
+
+def time_device(fn, reps=1):
+    """Device time (ms) of fn() on the current stream, after one warm call."""
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def other_configs(dev, hbm):
+    """BASELINE configs 1, 3, 4, 5, each run for its full n_t from zero fields
+    (the acoustic ones with zeroed levels inside the timing)."""
+    import paper_1608_03984_b200 as B
+    from paper_1608_03984_b200 import elastic, roofline as RL, tti
+    from paper_1608_03984_b200.synthetic import config1, config3
+
+    out = {}
+    fp32_peak = RL.b200_machine().peak_gflops_achievable
+    for name, cfg in (("config1", config1()), ("config3", config3())):
+        fld = B.Wavefield.allocate(cfg.dims, cfg.halo, device=dev)
+
+        def sim(c=cfg, f=fld):
+            for g in f.grids:
+                g.zero_()
+            f.it = 0
+            B.run(f, c)
+
+        ms = time_device(sim)
+        npts = float(np.prod(cfg.dims))
+        g = npts * cfg.n_t / (ms / 1e3) / 1e9
+        out[name] = {"workload": f"acoustic order {cfg.order}, {cfg.dims}, {cfg.n_t} steps",
+                     "gpts_per_s": round(g, 2), "ms_per_sim": round(ms, 3),
+                     "frac_hbm": round(g * 16 / hbm, 4), "bound": "hbm"}
+        del fld
+    cfg = tti.config4()
+    fld = tti.TTIWavefield.allocate(cfg.dims, cfg.halo, device=dev)
+
+    def sim4():
+        for g in fld.p + fld.r:
+            g.zero_()
+        fld.it = 0
+        tti.tti_run(fld, cfg)
+
+    ms = time_device(sim4)
+    g = float(np.prod(cfg.dims)) * cfg.n_t / (ms / 1e3) / 1e9
+    fl = tti.tti_flops_per_point(cfg.order)
+    out["config4"] = {"workload": f"TTI order 8, {cfg.dims}, {cfg.n_t} steps", "gpts_per_s": round(g, 2),
+                      "ms_per_sim": round(ms, 3), "gflops_catalog": round(g * fl, 1),
+                      "frac_fp32": round(g * fl / fp32_peak, 4), "bound": "fp32 (catalog OI 16.1)",
+                      "frac_hbm_60B": round(g * 60 / hbm, 4)}
+    del fld
+    cfg = elastic.config5()
+    fld = elastic.ElasticWavefield.allocate(cfg.dims, cfg.halo, device=dev)
+
+    def sim5():
+        for g in fld.fields:
+            g.zero_()
+        fld.it = 0
+        elastic.elastic_run(fld, cfg)
+
+    ms = time_device(sim5)
+    g = float(np.prod(cfg.dims)) * cfg.n_t / (ms / 1e3) / 1e9
+    out["config5"] = {"workload": f"elastic velocity-stress order 8, {cfg.dims}, {cfg.n_t} steps",
+                      "gpts_per_s": round(g, 2), "ms_per_sim": round(ms, 3),
+                      "frac_hbm_84B": round(g * 84 / hbm, 4), "bound": "hbm (84 B/pt)",
+                      "two_pass_gbs_120B": round(g * 120, 1)}
+    return out
 
 
 def load_ncu_traffic(order):
@@ -296,6 +373,10 @@ def main():
                           "gflops": round(g * RL.acoustic_flops_per_point(order), 1)})
             del f
 
+    configs = None
+    if rank == 0 and not args.no_configs:
+        configs = other_configs(dev, hbm)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args, cfg)
@@ -317,6 +398,7 @@ def main():
             "gpu_launches": launches_per_sim * args.steps,
             "clocks": clk.summary(),
             "per_order": sweep,
+            "baseline_configs": configs,
         }
         print(json.dumps(line), flush=True)
     if pg is not None:
