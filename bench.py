@@ -175,9 +175,11 @@ def cpu_baseline(args, cfg):
 
 
 def time_device(fn, reps=1):
-    """Device time (ms) of fn() on the current stream, after one warm call."""
+    """Device time (ms) of fn() on the current stream, after two warm calls
+    (the second captures the CUDA graph small runs replay)."""
     import torch
 
+    fn()
     fn()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
