@@ -103,6 +103,23 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def max_over_ranks(x, pg, device):
+    """The job's time is the slowest rank's device time (contract: max over ranks)."""
+    if pg is None:
+        return float(x)
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(world, per_rank_units, ms):
+    """Units all ranks processed / the max-over-ranks time, in G units/s (weak
+    scaling: every replica runs the full per-GPU workload)."""
+    return world * float(per_rank_units) / (ms / 1e3) / 1e9
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -313,13 +330,9 @@ def main():
         t_end.record(stream)
         t_end.synchronize()
     barrier()
-    ms = t_start.elapsed_time(t_end)
-    if pg is not None:
-        t = torch.tensor([ms], device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(t_start.elapsed_time(t_end), pg, dev)
     per_rank_pts = npts * cfg.n_t * args.steps
-    value = world * per_rank_pts / (ms / 1e3) / 1e9
+    value = whole_job_rate(world, per_rank_pts, ms)
 
     from paper_1608_03984_b200 import roofline as RL
 
@@ -343,12 +356,8 @@ def main():
         e1.record(stream)
         e1.synchronize()
         barrier()
-        ems = e0.elapsed_time(e1)
-        if pg is not None:
-            t = torch.tensor([ems], device=dev)
-            pg.all_reduce(t, op=pg.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": world * per_rank_pts / (ems / 1e3) / 1e9, "unit": UNIT,
+        ems = max_over_ranks(e0.elapsed_time(e1), pg, dev)
+        e2e = {"value": whole_job_rate(world, per_rank_pts, ems), "unit": UNIT,
                "h2d_bytes_per_step": sim.h2d_bytes, "d2h_bytes_per_step": sim.d2h_bytes,
                "ms_per_step": ems / args.steps}
         del sim
