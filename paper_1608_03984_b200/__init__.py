@@ -22,7 +22,8 @@ from .kernel import (
     run_benchmark,
     step,
 )
-from .roofline import MachineSpec, RooflinePoint, b200_machine, roofline_point
+from .roofline import (MachineSpec, RooflineDataset, RooflinePoint, b200_machine, get_machine,
+                       load_machines, roofline_dataset, roofline_point)
 from .stencils import a2_sum, acoustic_weights_f32, second_derivative_weights
 
 __version__ = "0.1.0"

@@ -13,7 +13,8 @@ derived FP32 peak of 148 SMs x 128 lanes x 2 FLOP x SM clock.
 
 import json
 import os
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
+from fractions import Fraction
 from typing import Optional
 
 from .errors import ValidationError
@@ -36,13 +37,66 @@ ACOUSTIC_BYTES_PER_POINT = 16  # m, u(t-2), u(t-1) read + u(t) written (equation
 
 
 @dataclass(frozen=True)
+class ArchParams:
+    """Core-side parameters of a machine document (machines.py:38-53)."""
+
+    simd_lanes_sp: int
+    fma_ops_per_cycle: int
+    cores: int
+    sockets: int
+    clock_ghz: float
+
+
+@dataclass(frozen=True)
+class MemParams:
+    """Memory-side parameters of a machine document (machines.py:56-67)."""
+
+    transfer_rate_mts: float
+    channels: int
+    bytes_per_channel: int
+    sockets: int
+
+
+def _exact(x) -> Fraction:
+    return Fraction(str(x))
+
+
+def theoretical_peak_flops(arch: ArchParams) -> float:
+    """lanes x fma x cores x sockets x clock in GFLOPS, in exact decimal
+    arithmetic (the reference's rule, machines.py:70-83)."""
+    return float(_exact(arch.simd_lanes_sp) * arch.fma_ops_per_cycle * arch.cores * arch.sockets
+                 * _exact(arch.clock_ghz))
+
+
+def theoretical_peak_bandwidth(mem: MemParams) -> float:
+    """transfer rate x channels x bytes x sockets in GB/s (machines.py:86-95)."""
+    return float(_exact(mem.transfer_rate_mts) * mem.channels * mem.bytes_per_channel
+                 * mem.sockets / 1000)
+
+
+@dataclass(frozen=True)
 class MachineSpec:
-    """Subset of fdroof.machines.MachineSpec (machines.py:98-148) used for reporting."""
+    """fdroof.machines.MachineSpec (machines.py:98-148): achievable peaks are
+    the roof; theoretical peaks, precision and provenance are carried along."""
 
     name: str
     peak_gflops_achievable: float
     peak_bw_achievable: float
     source: str = ""
+    peak_gflops_theoretical: Optional[float] = None
+    peak_bw_theoretical: Optional[float] = None
+    precision_bytes: int = 4
+    notes: str = ""
+    arch: Optional[ArchParams] = None
+    mem: Optional[MemParams] = None
+
+    def __post_init__(self):
+        if not (self.peak_gflops_achievable and self.peak_gflops_achievable > 0):
+            raise ValidationError(f"machine {self.name!r}: peak_gflops_achievable must be > 0")
+        if not (self.peak_bw_achievable and self.peak_bw_achievable > 0):
+            raise ValidationError(f"machine {self.name!r}: peak_bw_achievable must be > 0")
+        if self.precision_bytes not in (4, 8):
+            raise ValidationError(f"machine {self.name!r}: precision_bytes must be 4 or 8")
 
     @property
     def ridge_point(self) -> float:
@@ -50,6 +104,97 @@ class MachineSpec:
 
     def attainable(self, oi: float) -> float:
         return min(oi * self.peak_bw_achievable, self.peak_gflops_achievable)
+
+
+ACHIEVABLE_FRACTION_HINT = 0.8  # the reference's default when only theoretical peaks are given
+_MACHINE_KEYS = {"name", "peak_gflops_theoretical", "peak_bw_theoretical", "peak_gflops_achievable",
+                 "peak_bw_achievable", "precision_bytes", "notes", "arch", "mem"}
+_ARCH_KEYS = {"simd_lanes_sp", "fma_ops_per_cycle", "cores", "sockets", "clock_ghz"}
+_MEM_KEYS = {"transfer_rate_mts", "channels", "bytes_per_channel", "sockets"}
+MACHINES_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "machines")
+
+
+def _sub(doc, key, allowed, cls, where):
+    sub = doc.get(key)
+    if sub is None:
+        return None
+    if not isinstance(sub, dict):
+        raise ValidationError(f"{where}: '{key}' must be a mapping")
+    if set(sub) != allowed:
+        extra, missing = sorted(set(sub) - allowed), sorted(allowed - set(sub))
+        raise ValidationError(f"{where}: {key} keys: unknown {extra}, missing {missing}")
+    return cls(**sub)
+
+
+def machine_from_doc(doc, where="<doc>") -> MachineSpec:
+    """Validate one machine document with the reference's schema and rules
+    (machines.py:245-281): arch / mem give the theoretical peaks; missing
+    achievable peaks default to 80% of theoretical, noted in `notes`."""
+    if not isinstance(doc, dict):
+        raise ValidationError(f"{where}: machine document must be a mapping")
+    unknown = set(doc) - _MACHINE_KEYS
+    if unknown:
+        raise ValidationError(f"{where}: unknown machine keys: {sorted(unknown)}")
+    if "name" not in doc:
+        raise ValidationError(f"{where}: machine document missing 'name'")
+    arch = _sub(doc, "arch", _ARCH_KEYS, ArchParams, where)
+    mem = _sub(doc, "mem", _MEM_KEYS, MemParams, where)
+    theo_f = theoretical_peak_flops(arch) if arch else doc.get("peak_gflops_theoretical")
+    theo_b = theoretical_peak_bandwidth(mem) if mem else doc.get("peak_bw_theoretical")
+    ach_f, ach_b = doc.get("peak_gflops_achievable"), doc.get("peak_bw_achievable")
+    notes, defaulted = str(doc.get("notes", "")), []
+    if ach_f is None and theo_f is not None:
+        ach_f, _ = ACHIEVABLE_FRACTION_HINT * theo_f, defaulted.append("GFLOPS")
+    if ach_b is None and theo_b is not None:
+        ach_b, _ = ACHIEVABLE_FRACTION_HINT * theo_b, defaulted.append("bandwidth")
+    if defaulted:
+        hint = f"achievable {'/'.join(defaulted)} defaulted to 80% of theoretical"
+        notes = f"{notes}; {hint}" if notes else hint
+    if ach_f is None or ach_b is None:
+        raise ValidationError(f"{where}: machine needs achievable or theoretical peaks")
+    return MachineSpec(str(doc["name"]), float(ach_f), float(ach_b), where,
+                       None if theo_f is None else float(theo_f),
+                       None if theo_b is None else float(theo_b),
+                       int(doc.get("precision_bytes", 4)), notes, arch, mem)
+
+
+def load_machines(path) -> dict:
+    """All machine documents of a YAML file (multi-document), by name."""
+    import yaml
+
+    try:
+        with open(path, encoding="utf-8") as fh:
+            docs = [d for d in yaml.safe_load_all(fh) if d is not None]
+    except yaml.YAMLError as exc:
+        raise ValidationError(f"{path}: invalid YAML ({exc})") from None
+    out = {}
+    for i, d in enumerate(docs):
+        m = machine_from_doc(d, f"{path}[{i}]")
+        if m.name in out:
+            raise ValidationError(f"{path}: duplicate machine name {m.name!r}")
+        out[m.name] = m
+    return out
+
+
+def builtin_machines() -> dict:
+    out = {}
+    for fn in sorted(os.listdir(MACHINES_DIR)):
+        if fn.endswith((".yaml", ".yml")):
+            out.update(load_machines(os.path.join(MACHINES_DIR, fn)))
+    return out
+
+
+def get_machine(name: str = "b200", registry: Optional[dict] = None) -> MachineSpec:
+    """A machine by name from `registry` (default: the built-in documents).
+    For the built-in B200 the achievable bandwidth is the driver-measured copy
+    rate in MEASURED_PEAKS.json when that file is present."""
+    reg = registry if registry is not None else builtin_machines()
+    if name not in reg:
+        raise ValidationError(f"unknown machine {name!r}; known: {sorted(reg)}")
+    m = reg[name]
+    if registry is None and name == "b200":
+        return b200_machine()
+    return m
 
 
 @dataclass(frozen=True)
@@ -79,19 +224,71 @@ def measured_peaks(path: Optional[str] = None) -> dict:
         return {}
 
 
-def b200_machine(sm_mhz: Optional[float] = None) -> MachineSpec:
-    """B200 roofline: measured HBM copy GB/s and the derived FP32 GFLOPS."""
+def b200_machine(sm_mhz: Optional[float] = None, precision_bytes: int = 4) -> MachineSpec:
+    """B200 roofline from machines/b200.yaml: the measured HBM copy GB/s
+    (MEASURED_PEAKS.json) when present, the derived FP32 (or FP64: half rate)
+    GFLOPS at the given SM clock."""
+    doc = load_machines(os.path.join(MACHINES_DIR, "b200.yaml"))["b200"]
     peaks = measured_peaks()
     bw = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
     src = "measured (MEASURED_PEAKS.json)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     mhz = float(sm_mhz or peaks.get("sm_max_mhz", B200_MAX_SM_MHZ))
-    fp32 = B200_SMS * B200_FP32_LANES * 2 * mhz * 1e-3  # GFLOPS
-    return MachineSpec("b200", fp32, bw, src)
+    flops = B200_SMS * B200_FP32_LANES * 2 * mhz * 1e-3  # GFLOPS
+    if precision_bytes == 8:
+        flops /= 2.0  # B200 FP64 FMA rate: half the FP32 rate
+    return replace(doc, peak_gflops_achievable=flops, peak_bw_achievable=bw, source=src,
+                   precision_bytes=precision_bytes)
 
 
 def roofline_point(machine: MachineSpec, order: int,
-                   measured_gflops: Optional[float] = None) -> RooflinePoint:
+                   measured_gflops: Optional[float] = None,
+                   label: Optional[str] = None) -> RooflinePoint:
+    """analysis.py:170-181 for the acoustic kernel: OI = flops / (4 fields x
+    precision_bytes), attainable = min(OI B, F)."""
     k = order + 1
-    oi = acoustic_flops_per_point(order) / ACOUSTIC_BYTES_PER_POINT
+    oi = acoustic_flops_per_point(order) / (4 * machine.precision_bytes)
     bound = "memory" if oi < machine.ridge_point else "compute"
-    return RooflinePoint(f"acoustic:k{k}", oi, machine.attainable(oi), bound, k, measured_gflops)
+    return RooflinePoint(label or f"acoustic:k{k}", oi, machine.attainable(oi), bound, k,
+                         measured_gflops)
+
+
+@dataclass(frozen=True)
+class RooflineDataset:
+    """A machine's roof plus the points pinned against it (analysis.py:123-167)."""
+
+    machine: MachineSpec
+    points: tuple
+    oi_lo: float
+    oi_hi: float
+
+    def __post_init__(self):
+        if not (0 < self.oi_lo < self.oi_hi):
+            raise ValidationError(f"need 0 < oi_lo < oi_hi, got {self.oi_lo}, {self.oi_hi}")
+
+    @property
+    def ridge(self) -> float:
+        return self.machine.ridge_point
+
+    @property
+    def roof_segments(self):
+        """The bandwidth slope and the flat compute roof, meeting at the ridge."""
+        b, f = self.machine.peak_bw_achievable, self.machine.peak_gflops_achievable
+        return ((self.oi_lo, self.oi_lo * b), (self.ridge, f)), ((self.ridge, f), (self.oi_hi, f))
+
+    def inconsistencies(self, tolerance: float = 0.05):
+        """Points measured above their bound by more than `tolerance`."""
+        return [p for p in self.points if p.measured_gflops is not None
+                and p.measured_gflops > p.attainable_gflops * (1.0 + tolerance)]
+
+    def to_csv(self) -> str:
+        lines = ["label,k,oi,attainable_gflops,bound,measured_gflops"]
+        for p in self.points:
+            m = "" if p.measured_gflops is None else repr(float(p.measured_gflops))
+            lines.append(f"{p.label},{p.k},{p.oi!r},{p.attainable_gflops!r},{p.bound},{m}")
+        return "\n".join(lines) + "\n"
+
+
+def roofline_dataset(machine: MachineSpec, points, margin: float = 10.0) -> RooflineDataset:
+    """Dataset spanning the points and the ridge with a factor `margin` each side."""
+    ois = [p.oi for p in points] + [machine.ridge_point]
+    return RooflineDataset(machine, tuple(points), min(ois) / margin, max(ois) * margin)
