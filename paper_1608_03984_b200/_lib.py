@@ -63,6 +63,41 @@ class AcousticArgs(ctypes.Structure):
     ]
 
 
+class Acoustic64Args(ctypes.Structure):
+    """Mirror of `fdr_acoustic64_args` (include/b200fd.h): the float64 step."""
+
+    _fields_ = [
+        ("abi_version", _i32),
+        ("order", _i32),
+        ("nx", _i32),
+        ("ny", _i32),
+        ("nz", _i32),
+        ("pitch_y", _i32),
+        ("pitch_x", ctypes.c_int64),
+        ("weights", ctypes.c_double * (MAX_RADIUS + 1)),
+        ("coef", ctypes.c_double),
+        ("m_mode", _i32),
+        ("m_scalar", ctypes.c_double),
+        ("m", _vp),
+        ("levels", _vp * 3),
+        ("sponge_x", _vp),
+        ("sponge_y", _vp),
+        ("sponge_z", _vp),
+        ("series", _vp),
+        ("n_series", _i32),
+        ("src_x", _i32),
+        ("src_y", _i32),
+        ("src_z", _i32),
+        ("n_rec", _i32),
+        ("rec_xyz", _vp),
+        ("traces", _vp),
+        ("trace_rows", _i32),
+        ("it0", _i32),
+        ("n_steps", _i32),
+        ("variant", _i32),
+    ]
+
+
 # Every symbol include/b200fd.h declares: (name, restype, argtypes).
 EXPORTS = (
     ("fdr_abi_version", ctypes.c_int, ()),
@@ -82,6 +117,8 @@ EXPORTS = (
     ("fdr_tti_run", ctypes.c_int, (ctypes.c_void_p, _vp)),
     ("fdr_elastic_args_size", ctypes.c_size_t, ()),
     ("fdr_elastic_run", ctypes.c_int, (ctypes.c_void_p, _vp)),
+    ("fdr_acoustic64_args_size", ctypes.c_size_t, ()),
+    ("fdr_acoustic64_run", ctypes.c_int, (ctypes.POINTER(Acoustic64Args), _vp)),
     ("fdr_selftest_division", ctypes.c_int64,
      (ctypes.c_int64, ctypes.c_float, ctypes.c_float, ctypes.c_uint32,
       ctypes.POINTER(ctypes.c_int64))),
@@ -115,6 +152,8 @@ def load():
             )
         if lib.fdr_acoustic_args_size() != ctypes.sizeof(AcousticArgs):
             raise ExtensionMissingError("fdr_acoustic_args layout mismatch between header and binding")
+        if lib.fdr_acoustic64_args_size() != ctypes.sizeof(Acoustic64Args):
+            raise ExtensionMissingError("fdr_acoustic64_args layout mismatch between header and binding")
         _lib = lib
         return lib
 

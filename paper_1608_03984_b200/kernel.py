@@ -176,6 +176,10 @@ class Wavefield:
     (the kernels read zeros outside the interior), so `halo` records the
     width a host copy is padded with.  `traces` holds receiver samples,
     shape (rows, n_rec), when the config has receivers.
+
+    Levels allocated with dtype=torch.float64 select the float64 path
+    (fdr_acoustic64_run): the same update sequence in IEEE
+    double, for measuring the float32 path's rounding error.
     """
 
     def __init__(self, halo: int, grids: list, dims: tuple, it: int = 0):
@@ -186,16 +190,27 @@ class Wavefield:
         self.traces = None
 
     @classmethod
-    def allocate(cls, dims, halo: int, device=None) -> "Wavefield":
+    def allocate(cls, dims, halo: int, device=None, dtype=None) -> "Wavefield":
         if len(dims) != 3 or any(d < 2 * halo + 1 for d in dims):
             raise ValidationError(f"dims {tuple(dims)} too small for halo width {halo}")
         torch = _torch()
         _lib.load()
+        dtype = torch.float32 if dtype is None else dtype
+        if dtype not in (torch.float32, torch.float64):
+            raise ValidationError(f"wavefield dtype must be float32 or float64, got {dtype}")
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         nx, ny, nz = (int(d) for d in dims)
         shape = (nx, ny, row_pitch(nz))
-        grids = [torch.zeros(shape, dtype=torch.float32, device=dev) for _ in range(3)]
+        grids = [torch.zeros(shape, dtype=dtype, device=dev) for _ in range(3)]
         return cls(halo, grids, (nx, ny, nz))
+
+    @property
+    def dtype(self):
+        return self.grids[0].dtype
+
+    @property
+    def _np_dtype(self):
+        return np.float64 if self.dtype == _torch().float64 else np.float32
 
     @property
     def dims(self):
@@ -210,12 +225,12 @@ class Wavefield:
         return self.grids[level][:, :, : self._dims[2]]
 
     def numpy(self, level: int = 2) -> np.ndarray:
-        """Host copy of a level's interior as float32, C order."""
+        """Host copy of a level's interior (float32, or float64 levels), C order."""
         return self.interior(level).cpu().numpy().copy()
 
     def set_interior(self, level: int, values) -> None:
         torch = _torch()
-        arr = np.ascontiguousarray(np.asarray(values, dtype=np.float32))
+        arr = np.ascontiguousarray(np.asarray(values, dtype=self._np_dtype))
         if arr.shape != self._dims:
             raise ValidationError(f"interior values of shape {arr.shape} do not match dims {self._dims}")
         self.interior(level).copy_(torch.from_numpy(arr))
@@ -231,7 +246,7 @@ class Wavefield:
         r = self.halo
         out = []
         for lvl in range(3):
-            padded = np.zeros(tuple(d + 2 * r for d in self._dims), dtype=np.float32)
+            padded = np.zeros(tuple(d + 2 * r for d in self._dims), dtype=self._np_dtype)
             padded[r : r + self._dims[0], r : r + self._dims[1], r : r + self._dims[2]] = self.numpy(lvl)
             out.append(padded)
         return out
@@ -241,9 +256,11 @@ class Wavefield:
         """Upload a reference-layout Wavefield (three padded numpy levels)."""
         r = int(halo)
         dims = tuple(s - 2 * r for s in np.shape(grids[0]))
-        fld = cls.allocate(dims, r, device)
+        torch = _torch()
+        f64 = np.asarray(grids[0]).dtype == np.float64
+        fld = cls.allocate(dims, r, device, torch.float64 if f64 else torch.float32)
         for lvl in range(3):
-            g = np.asarray(grids[lvl], dtype=np.float32)
+            g = np.asarray(grids[lvl], dtype=fld._np_dtype)
             fld.set_interior(lvl, g[r : r + dims[0], r : r + dims[1], r : r + dims[2]])
         fld.it = int(it)
         return fld
@@ -357,9 +374,14 @@ def run(fld: Wavefield, cfg: KernelConfig, n_steps: Optional[int] = None,
     torch = _torch()
     lib = _lib.load()
     dev = fld.device
+    dt0 = fld.grids[0].dtype
     for g in fld.grids:
-        if g.dtype != torch.float32 or not g.is_cuda or not g.is_contiguous() or g.shape != fld.grids[0].shape:
-            raise ValidationError("wavefield levels must be contiguous float32 CUDA tensors of one shape")
+        if (g.dtype != dt0 or dt0 not in (torch.float32, torch.float64) or not g.is_cuda
+                or not g.is_contiguous() or g.shape != fld.grids[0].shape):
+            raise ValidationError("wavefield levels must be contiguous float32 (or float64) CUDA "
+                                  "tensors of one shape and dtype")
+    if dt0 == torch.float64:
+        return _run_f64(fld, cfg, n, variant)
     pitch_y = int(fld.grids[0].shape[2])
     pitch_x = int(fld.grids[0].shape[1]) * pitch_y
     plan = _plan(cfg, dev, pitch_y)
@@ -390,6 +412,102 @@ def run(fld: Wavefield, cfg: KernelConfig, n_steps: Optional[int] = None,
         _lib.check(lib.fdr_acoustic_run(ctypes.byref(args), ctypes.c_void_p(stream)))
     g = fld.grids
     fld.grids = [g[n % 3], g[(1 + n) % 3], g[(2 + n) % 3]]  # kernel.py:219, n times
+    fld.it += n
+    return fld
+
+
+class _DevicePlan64:
+    """Device-resident float64 constants of a config for the float64 path:
+    weights 3 w0 and w_j in double, coef = dt*dt/(h*h) in double, m, sponge
+    and series converted exactly to double."""
+
+    def __init__(self, cfg: KernelConfig, device, pitch: int):
+        torch = _torch()
+        self.key = _plan_key(cfg, device)
+        self.refs = (cfg.m, cfg.source, cfg.receivers, cfg.sponge)
+        nx, ny, nz = cfg.dims
+        r = cfg.order // 2
+        w = [float(x) for x in second_derivative_weights(cfg.order)]
+        self.weights = [3.0 * w[r]] + [w[r + j] for j in range(1, r + 1)]
+        self.coef = cfg.dt * cfg.dt / (cfg.h * cfg.h)
+        self.m_grid = None
+        self.m_scalar = 1.0
+        if np.isscalar(cfg.m):
+            self.m_scalar = float(cfg.m)
+            self.m_mode = _lib.M_NONE if self.m_scalar == 1.0 else _lib.M_SCALAR
+        else:
+            self.m_mode = _lib.M_GRID
+            host = np.ascontiguousarray(np.asarray(cfg.m, dtype=np.float64))
+            self.m_grid = torch.zeros((nx, ny, pitch), dtype=torch.float64, device=device)
+            self.m_grid[:, :, :nz].copy_(torch.from_numpy(host))
+        self.sponge = None
+        if cfg.sponge is not None:
+            self.sponge = tuple(torch.from_numpy(np.asarray(p, dtype=np.float64)).to(device)
+                                for p in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
+        self.series = None
+        self.src = (-1, 0, 0)
+        if cfg.source is not None:
+            series = np.ascontiguousarray(np.asarray(cfg.source.series, dtype=np.float64).reshape(-1))
+            self.series = torch.from_numpy(series).to(device)
+            self.src = tuple(int(c) for c in cfg.source.location)
+        self.n_series = 0 if self.series is None else int(self.series.numel())
+        self.rec = None
+        if cfg.receivers is not None:
+            self.rec = torch.from_numpy(cfg.receivers.locations.reshape(-1).copy()).to(device)
+
+
+def _run_f64(fld: Wavefield, cfg: KernelConfig, n: int, variant: str) -> Wavefield:
+    """The float64 path of `run` (fdr_acoustic64_run)."""
+    torch = _torch()
+    lib = _lib.load()
+    dev = fld.device
+    if variant == "tma":
+        raise ValidationError("the float64 path has variants auto, queue and direct")
+    pitch_y = int(fld.grids[0].shape[2])
+    pitch_x = int(fld.grids[0].shape[1]) * pitch_y
+    plan = getattr(cfg, "_device_plan64", None)
+    if (plan is None or plan.key != _plan_key(cfg, dev)
+            or (plan.m_grid is not None and tuple(plan.m_grid.shape) != tuple(fld.grids[0].shape))):
+        plan = _DevicePlan64(cfg, dev, pitch_y)
+        cfg._device_plan64 = plan
+    a = _lib.Acoustic64Args()
+    a.abi_version = _lib.ABI_VERSION
+    a.order = cfg.order
+    a.nx, a.ny, a.nz = fld.dims
+    a.pitch_y, a.pitch_x = pitch_y, pitch_x
+    for j, w in enumerate(plan.weights):
+        a.weights[j] = w
+    a.coef = plan.coef
+    a.m_mode = plan.m_mode
+    a.m_scalar = plan.m_scalar
+    a.m = _ptr(plan.m_grid)
+    for i in range(3):
+        a.levels[i] = fld.grids[i].data_ptr()
+    if plan.sponge is not None:
+        a.sponge_x, a.sponge_y, a.sponge_z = (p.data_ptr() for p in plan.sponge)
+    a.series = _ptr(plan.series)
+    a.n_series = plan.n_series
+    a.src_x, a.src_y, a.src_z = plan.src
+    a.n_rec = 0 if cfg.receivers is None else cfg.receivers.count
+    if plan.rec is not None:
+        rows = max(cfg.n_t, fld.it + n)
+        if fld.traces is None or fld.traces.dtype != torch.float64 or fld.traces.shape[0] < rows \
+                or fld.traces.shape[1] != a.n_rec:
+            grown = torch.zeros((rows, a.n_rec), dtype=torch.float64, device=dev)
+            if fld.traces is not None and fld.traces.shape[1] == a.n_rec:
+                grown[: fld.traces.shape[0]].copy_(fld.traces)
+            fld.traces = grown
+        a.rec_xyz = plan.rec.data_ptr()
+        a.traces = fld.traces.data_ptr()
+        a.trace_rows = int(fld.traces.shape[0])
+    a.it0 = fld.it
+    a.n_steps = n
+    a.variant = _VARIANTS[variant]
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        _lib.check(lib.fdr_acoustic64_run(ctypes.byref(a), ctypes.c_void_p(stream)))
+    g = fld.grids
+    fld.grids = [g[n % 3], g[(1 + n) % 3], g[(2 + n) % 3]]
     fld.it += n
     return fld
 
