@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--no-fp64", action="store_true", help="skip the float64 leg")
     p.add_argument("--no-configs", action="store_true",
                    help="skip the BASELINE configs 1, 3, 4, 5 lines")
     return p.parse_args()
@@ -268,6 +269,32 @@ def other_configs(dev, hbm):
     return out
 
 
+def fp64_leg(dev, cfg, hbm, final32):
+    """the config-2 simulation in float64 (fdr_acoustic64_run),
+    timed on the device, and the float32 headline's final wavefield's relative
+    L2 error against it."""
+    import torch
+
+    import paper_1608_03984_b200 as B
+
+    fld = B.Wavefield.allocate(cfg.dims, cfg.halo, device=dev, dtype=torch.float64)
+
+    def sim():
+        for g in fld.grids:
+            g.zero_()
+        fld.it = 0
+        B.run(fld, cfg)
+
+    ms = time_device(sim)
+    g = float(np.prod(cfg.dims)) * cfg.n_t / (ms / 1e3) / 1e9
+    ref = fld.interior(2).double()
+    err = float(torch.linalg.vector_norm(final32.double() - ref) / torch.linalg.vector_norm(ref))
+    return {"workload": f"acoustic order {cfg.order}, {tuple(cfg.dims)}, {cfg.n_t} steps, float64",
+            "gpts_per_s": round(g, 2), "ms_per_sim": round(ms, 3), "bytes_per_point": 32,
+            "frac_hbm": round(g * 32 / hbm, 4), "kernel": f"a64_stream<R={cfg.order // 2}>",
+            "f32_rel_l2_vs_f64": err}
+
+
 def load_ncu_traffic(order):
     """DRAM bytes per launch of the step kernel from the committed ncu capture
     (profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum)."""
@@ -384,6 +411,12 @@ def main():
                           "gflops": round(g * RL.acoustic_flops_per_point(order), 1)})
             del f
 
+    fp64 = None
+    if rank == 0 and not args.no_fp64:
+        one_sim()
+        torch.cuda.synchronize(dev)
+        fp64 = fp64_leg(dev, cfg, hbm, fld.interior(2))
+
     configs = None
     if rank == 0 and not args.no_configs:
         configs = other_configs(dev, hbm)
@@ -410,6 +443,7 @@ def main():
             "clocks": clk.summary(),
             "per_order": sweep,
             "baseline_configs": configs,
+            "fp64": fp64,
         }
         print(json.dumps(line), flush=True)
     if pg is not None:

@@ -12,7 +12,7 @@
 // parity oracle is oracle/acoustic.py's numpy restatement run on float64
 // levels (tests/test_fp64.py).
 //
-// a64_stream: a 32(z) x 16(y) tile of one point per thread streams along x.
+// a64_stream: a 32(z) x 8(y) tile of one point per thread streams along x.
 // The 2r+1 x-neighbours of a thread's column live in a register queue; the
 // y/z taps read a shared-memory box of the centre plane (zero halo written
 // explicitly), double-buffered: the box of plane x+1, the queue's next value
@@ -119,13 +119,16 @@ __global__ void __launch_bounds__(256) a64_direct(const A64Step a) {
   a.out[p] = finish(a, c, a.prev[p], lap, a.m_mode == FDR_M_GRID ? a.m[p] : 1.0, g, src);
 }
 
-constexpr int TZ = 32, TY = 16, NT = TZ * TY;
+#ifndef FDR64_TY
+#define FDR64_TY 8
+#endif
+constexpr int TZ = 32, TY = FDR64_TY, NT = TZ * TY;
 
 template <int R>
 struct Geo {
   static constexpr int BZ = TZ + 2 * R, BY = TY + 2 * R, BOX = BZ * BY;
   static constexpr int NL = (BOX + NT - 1) / NT;  // box elements per thread
-  static constexpr int MINB = R <= 4 ? 2 : 1;
+  static constexpr int MINB = R <= 4 ? 2 * (512 / NT) : 512 / NT;
 };
 
 template <int R, bool SPONGE>
@@ -137,56 +140,61 @@ __global__ void __launch_bounds__(NT, Geo<R>::MINB) a64_stream(const A64Step a) 
   const int zt = blockIdx.x * TZ, yt = blockIdx.y * TY;
   const int z = zt + tz, y = yt + ty;
   const int xb = blockIdx.z * a.chunk;
-  const int xe = min(a.nx, xb + a.chunk);
+  const int nx = a.nx;
+  const int xe = min(nx, xb + a.chunk);
   if (xb >= xe) return;
   const bool inb = z < a.nz && y < a.ny;
-  const size_t px = (size_t)a.pitch_x;
-  const size_t own = (size_t)y * a.pitch_y + z;
-  auto col = [&](const double* p, int x) -> double {
-    return (inb && x >= 0 && x < a.nx) ? p[(size_t)x * px + own] : 0.0;
-  };
-  // box element e of plane x (zero outside the interior: the reference halo)
-  auto box_load = [&](int x, double* v) {
+  const long long px = a.pitch_x;
+  const int own = inb ? y * a.pitch_y + z : 0;
+  // loop-invariant box element offsets within a plane (-1: outside, reads 0)
+  int boff[G::NL];
 #pragma unroll
-    for (int l = 0; l < G::NL; ++l) {
-      const int e = tid + l * NT;
-      double val = 0.0;
-      if (e < G::BOX) {
-        const int by = e / G::BZ, bz = e - by * G::BZ;
-        const int gy = yt - R + by, gz = zt - R + bz;
-        if (gy >= 0 && gy < a.ny && gz >= 0 && gz < a.nz)
-          val = a.cur[(size_t)x * px + (size_t)gy * a.pitch_y + gz];
-      }
-      v[l] = val;
-    }
-  };
-  auto box_store = [&](int buf, const double* v) {
-#pragma unroll
-    for (int l = 0; l < G::NL; ++l)
-      if (tid + l * NT < G::BOX) box[buf][tid + l * NT] = v[l];
-  };
+  for (int l = 0; l < G::NL; ++l) {
+    const int e = tid + l * NT;
+    const int by = e / G::BZ, bz = e - by * G::BZ;
+    const int gy = yt - R + by, gz = zt - R + bz;
+    boff[l] = (e < G::BOX && gy >= 0 && gy < a.ny && gz >= 0 && gz < a.nz) ? gy * a.pitch_y + gz : -1;
+  }
   const double gyv = (SPONGE && inb) ? a.gy[y] : 1.0, gzv = (SPONGE && inb) ? a.gz[z] : 1.0;
   const bool src_col = inb && y == a.sy && z == a.sz && a.it < a.n_series;
+  const int sx = src_col ? a.sx : -1;
+  const bool grid_m = a.m_mode == FDR_M_GRID;
 
+  // column pointers at plane xb; they advance one plane per iteration
+  const double* cur0 = a.cur + own;
   double q[2 * R + 1];
 #pragma unroll
-  for (int i = 0; i < 2 * R; ++i) q[i] = col(a.cur, xb - R + i);
+  for (int i = 0; i < 2 * R; ++i) {
+    const int x = xb - R + i;
+    q[i] = (inb && x >= 0 && x < nx) ? cur0[x * px] : 0.0;
+  }
+  const double* lead_p = cur0 + (xb + R) * px;       // queue head: plane x + R
+  const double* plane_p = a.cur + xb * px;           // box source: plane x
+  const double* prev_p = a.prev + own + xb * px;
+  const double* m_p = (grid_m ? a.m : a.cur) + own + xb * px;
+  double* out_p = a.out + own + xb * px;
   double bv[G::NL];
-  box_load(xb, bv);
-  box_store(0, bv);
-  double lead = col(a.cur, xb + R);
+#pragma unroll
+  for (int l = 0; l < G::NL; ++l) bv[l] = boff[l] >= 0 ? plane_p[boff[l]] : 0.0;
+#pragma unroll
+  for (int l = 0; l < G::NL; ++l)
+    if (tid + l * NT < G::BOX) box[0][tid + l * NT] = bv[l];
+  double lead = (inb && xb + R < nx) ? *lead_p : 0.0;
   __syncthreads();
   const int cbox = (ty + R) * G::BZ + tz + R;
 #pragma unroll 1
   for (int x = xb, i = 0; x < xe; ++x, ++i) {
     q[2 * R] = lead;
     const bool more = x + 1 < xe;
+    plane_p += px;
+    lead_p += px;
     if (more) {
-      box_load(x + 1, bv);
-      lead = col(a.cur, x + 1 + R);
+#pragma unroll
+      for (int l = 0; l < G::NL; ++l) bv[l] = boff[l] >= 0 ? plane_p[boff[l]] : 0.0;
+      lead = (inb && x + 1 + R < nx) ? *lead_p : 0.0;
     }
-    const double pv = col(a.prev, x);
-    const double mv = a.m_mode == FDR_M_GRID ? col(a.m, x) : 1.0;
+    const double pv = inb ? *prev_p : 0.0;
+    const double mv = (grid_m && inb) ? *m_p : 1.0;
     const double* b = box[i & 1];
     const double c = q[R];
     double lap = __dmul_rn(a.w[0], c);
@@ -198,11 +206,18 @@ __global__ void __launch_bounds__(NT, Geo<R>::MINB) a64_stream(const A64Step a) 
     for (int j = 1; j <= R; ++j) lap = tapd(lap, a.w[j], b[cbox + j], b[cbox - j]);
     if (inb) {
       const double g = SPONGE ? __dmul_rn(__dmul_rn(__ldg(a.gx + x), gyv), gzv) : 1.0;
-      a.out[(size_t)x * px + own] = finish(a, c, pv, lap, mv, g, src_col && x == a.sx);
+      *out_p = finish(a, c, pv, lap, mv, g, x == sx);
     }
+    prev_p += px;
+    m_p += px;
+    out_p += px;
 #pragma unroll
     for (int k = 0; k < 2 * R; ++k) q[k] = q[k + 1];
-    if (more) box_store((i + 1) & 1, bv);
+    if (more) {
+#pragma unroll
+      for (int l = 0; l < G::NL; ++l)
+        if (tid + l * NT < G::BOX) box[(i + 1) & 1][tid + l * NT] = bv[l];
+    }
     __syncthreads();
   }
 }
