@@ -252,7 +252,11 @@ static int run(const fdr_elastic_args* a, cudaStream_t st) {
 // sums are formed on arrival and delayed R planes in registers; the x
 // derivatives read register windows of own-column values.  Stages are
 // recycled by the last warp to release them (empty mbarrier).
-constexpr int ETZ = 32, ETY = 16, ENT = ETZ * ETY;
+#ifndef FDR_EL_TY
+#define FDR_EL_TY 8
+#endif
+constexpr int ETZ = 32, ETY = FDR_EL_TY, ENT = ETZ * ETY;
+constexpr int EMINB = ETY <= 8 ? 2 : 1;  // CTAs per SM the tile is sized for
 
 template <int R, int NBOX, int NTILE>
 struct EGeo {
@@ -319,7 +323,7 @@ FDR_DEV float wB(const float* w, int c, const float* cc) {
 // PASS 0: velocity (boxes sxy sxz syy syz szz; tiles sxx [newest], vx vy vz bs [centre])
 // PASS 1: stress   (boxes vx vy vz;            tiles sxx syy szz sxy sxz syz lam mu [centre])
 template <int R, int PASS, bool SPONGE>
-__global__ void __launch_bounds__(ENT, 1) el_stream(const __grid_constant__ ElMaps maps,
+__global__ void __launch_bounds__(ENT, EMINB) el_stream(const __grid_constant__ ElMaps maps,
                                                     const ElStep a) {
   constexpr int NBOX = PASS == 0 ? 5 : 3;
   constexpr int NTILE = PASS == 0 ? 5 : 8;
@@ -579,7 +583,8 @@ static int el_step_r(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st
     int dev = 0;
     EL_CUDA(cudaGetDevice(&dev));
     EL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const long tiles = (long)((a->nz + ETZ - 1) / ETZ) * ((a->ny + ETY - 1) / ETY), slots = nsm;
+    const long tiles = (long)((a->nz + ETZ - 1) / ETZ) * ((a->ny + ETY - 1) / ETY),
+               slots = (long)nsm * EMINB;
     double best = 1e30;
     int best_c = 1;
     for (int c = 1; c <= std::max(1, a->nx / (2 * R)); ++c) {

@@ -174,7 +174,11 @@ __global__ void tti_gather_kernel(const float* p, const int* rec, int n_rec, flo
 // shared memory.  Stages are recycled by the last warp to release them (empty
 // mbarrier, as in acoustic_queue); one __syncthreads per plane orders the
 // D1z buffer.
-constexpr int TTZ = 32, TTY = 16, TNT = TTZ * TTY;
+#ifndef FDR_TTI_TY
+#define FDR_TTI_TY 16
+#endif
+constexpr int TTZ = 32, TTY = FDR_TTI_TY, TNT = TTZ * TTY;
+constexpr int TMINB = TTY <= 8 ? 2 : 1;  // CTAs per SM the tile is sized for
 
 template <int R>
 struct TGeo {
@@ -225,7 +229,7 @@ FDR_DEV float d1_row(const float* row, const float* w1) {  // D1 along z at row[
 }
 
 template <int R, bool SPONGE>
-__global__ void __launch_bounds__(TNT, 1) tti_stream(const __grid_constant__ TTIMaps maps,
+__global__ void __launch_bounds__(TNT, TMINB) tti_stream(const __grid_constant__ TTIMaps maps,
                                                      const TTIStep a) {
   using G = TGeo<R>;
   extern __shared__ __align__(128) float smem[];
