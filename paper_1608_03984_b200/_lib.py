@@ -112,6 +112,18 @@ EXPORTS = (
         (ctypes.POINTER(AcousticArgs), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
          ctypes.c_size_t, _vp),
     ),
+    (
+        "fdr_acoustic_run_host_async",
+        ctypes.c_int,
+        (ctypes.POINTER(AcousticArgs), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+         ctypes.c_size_t, _vp),
+    ),
+    ("fdr_acoustic_host_upload", ctypes.c_int,
+     (ctypes.POINTER(AcousticArgs), _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp)),
+    ("fdr_acoustic_host_run_ws", ctypes.c_int,
+     (ctypes.POINTER(AcousticArgs), ctypes.c_int, _vp, ctypes.c_size_t, _vp)),
+    ("fdr_acoustic_host_download", ctypes.c_int,
+     (ctypes.POINTER(AcousticArgs), ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t, _vp)),
     ("fdr_last_launch_count", ctypes.c_int64, ()),
     ("fdr_tti_args_size", ctypes.c_size_t, ()),
     ("fdr_tti_run", ctypes.c_int, (ctypes.c_void_p, _vp)),

@@ -667,6 +667,103 @@ class HostSimulation:
         return self.h_final.numpy(), traces
 
 
+    def _slot(self, k: int):
+        """(workspace pointer, pinned final, pinned traces) of pipeline slot k;
+        slot 0 reuses the synchronous `run`'s buffers."""
+        torch = _torch()
+        if not hasattr(self, "_slots"):
+            self._slots = []
+            self._streams = tuple(torch.cuda.Stream(self.device) for _ in range(3))
+        while len(self._slots) <= k:
+            if not self._slots:
+                keep, ws, hf, ht = None, self.ws_ptr, self.h_final, self.h_traces
+            else:
+                keep = torch.empty(self.ws_bytes + 256, dtype=torch.uint8, device=self.device)
+                ws = (keep.data_ptr() + 255) // 256 * 256
+                hf = torch.empty_like(self.h_final).pin_memory()
+                ht = torch.empty_like(self.h_traces).pin_memory()
+            self._slots.append((ws, hf, ht, keep))
+        return self._slots[k][:3]
+
+    def run_pipelined(self, n_sims: int, depth: int = 2, on_result=None):
+        """`n_sims` back-to-back simulations (shots), each uploading all its
+        inputs and downloading its final level and traces, with `depth`
+        workspaces: the time steps run in order on one compute stream while
+        shot i+1's upload and shot i's download run on two copy streams
+        (fdr_acoustic_host_upload / _run_ws / _download), so the copies hide
+        behind the steps.  Ordered after the caller's current stream, which
+        waits for all of it: CUDA events on that stream time the whole batch.
+        on_result(i, final, traces) receives each shot's host results (copies).
+        Returns the last shot's (final, traces) as views of the pinned output
+        buffers, valid until the next run (as `run` does).
+        """
+        torch = _torch()
+        if n_sims < 1 or depth < 1:
+            raise ValidationError("need n_sims >= 1 and depth >= 1")
+        lib = self.lib
+        cur = torch.cuda.current_stream(self.device)
+        self._slot(depth - 1)
+        up, comp, down = self._streams
+        start = torch.cuda.Event()
+        start.record(cur)
+        for st in (up, comp, down):
+            st.wait_event(start)
+        p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        sx, sy, sz = (None, None, None) if self.h_sponge is None else tuple(p(t) for t in self.h_sponge)
+        has_rec = self.cfg.receivers is not None
+        args = ctypes.byref(self.args)
+        comp_done, down_done = [None] * n_sims, [None] * n_sims
+        delivered = set()
+
+        def deliver(i):
+            if on_result is not None and i not in delivered:
+                down_done[i].synchronize()
+                on_result(i, *self._host_results(*self._slot(i % depth)[1:]))
+                delivered.add(i)
+
+        with torch.cuda.device(self.device):
+            for i in range(n_sims):
+                ws, hf, ht = self._slot(i % depth)
+                if i >= depth:
+                    up.wait_event(comp_done[i - depth])  # slot inputs no longer read
+                _lib.check(lib.fdr_acoustic_host_upload(args, p(self.h_m), sx, sy, sz, p(self.h_series),
+                                                        p(self.h_rec), ctypes.c_void_p(ws), self.ws_bytes,
+                                                        ctypes.c_void_p(up.cuda_stream)))
+                ev = torch.cuda.Event()
+                ev.record(up)
+                comp.wait_event(ev)
+                if i >= depth:
+                    comp.wait_event(down_done[i - depth])  # slot levels downloaded
+                newest = _lib.check(lib.fdr_acoustic_host_run_ws(args, int(self.h_sponge is not None),
+                                                                 ctypes.c_void_p(ws), self.ws_bytes,
+                                                                 ctypes.c_void_p(comp.cuda_stream)))
+                comp_done[i] = torch.cuda.Event()
+                comp_done[i].record(comp)
+                down.wait_event(comp_done[i])
+                if i >= depth:
+                    deliver(i - depth)  # before its pinned buffers are overwritten
+                _lib.check(lib.fdr_acoustic_host_download(args, newest, p(hf), p(ht) if has_rec else None,
+                                                          ctypes.c_void_p(ws), self.ws_bytes,
+                                                          ctypes.c_void_p(down.cuda_stream)))
+                down_done[i] = torch.cuda.Event()
+                down_done[i].record(down)
+        cur.wait_event(down_done[-1])
+        for i in range(max(0, n_sims - depth), n_sims):
+            deliver(i)
+        down_done[-1].synchronize()
+        hf, ht = self._slot((n_sims - 1) % depth)[1:]
+        traces = None
+        if has_rec:
+            traces = ht.numpy()[: self.cfg.n_t, : self.cfg.receivers.count]
+        return hf.numpy(), traces  # views of the pinned buffers, like run()
+
+    def _host_results(self, hf, ht):
+        traces = None
+        if self.cfg.receivers is not None:
+            traces = ht.numpy()[: self.cfg.n_t, : self.cfg.receivers.count].copy()
+        return hf.numpy().copy(), traces
+
+
 class _HostPlan:
     """Host-side float32 constants of a config (same casts as _DevicePlan)."""
 
