@@ -35,7 +35,7 @@ from .roofline import (
 from .stencils import abs_sum, acoustic_weights_f32, second_derivative_weights
 
 _VARIANTS = {"auto": _lib.VARIANT_AUTO, "direct": _lib.VARIANT_DIRECT, "tma": _lib.VARIANT_TMA,
-             "queue": _lib.VARIANT_QUEUE}
+             "queue": _lib.VARIANT_QUEUE, "persistent": _lib.VARIANT_PERSISTENT}
 
 
 def _torch():

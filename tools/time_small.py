@@ -15,7 +15,7 @@ def main():
 
     for dims in ((64, 64, 64), (96, 96, 96), (128, 128, 128), (192, 192, 192)):
         cfg = config1(dims=dims)
-        for variant in ("queue", "direct"):
+        for variant in ("queue", "direct", "persistent"):
             fld = B.Wavefield.allocate(cfg.dims, cfg.halo)
 
             def sim():
