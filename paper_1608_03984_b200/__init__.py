@@ -16,7 +16,10 @@ from .kernel import (
     Sponge,
     StabilityWarning,
     Wavefield,
+    dump_traces,
     dump_wavefield,
+    load_traces,
+    load_wavefield,
     max_stable_dt,
     run,
     run_benchmark,

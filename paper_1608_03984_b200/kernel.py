@@ -597,6 +597,46 @@ def dump_wavefield(fld: Wavefield, path) -> None:
         fh.write(f"{nx} {ny} {nz}\n")
 
 
+def load_wavefield(path) -> np.ndarray:
+    """Read a `dump_wavefield` file back: (nx, ny, nz) float32 from the
+    x-fastest little-endian data and the `nx ny nz` sidecar (kernel.py:293-301)."""
+    with open(f"{path}.dims", encoding="utf-8") as fh:
+        dims = tuple(int(v) for v in fh.read().split())
+    if len(dims) != 3:
+        raise ValidationError(f"{path}.dims: expected 'nx ny nz'")
+    data = np.fromfile(path, dtype="<f4")
+    if data.size != int(np.prod(dims)):
+        raise ValidationError(f"{path}: {data.size} values, sidecar says {dims}")
+    return data.reshape(dims, order="F").astype(np.float32)
+
+
+def dump_traces(fld: Wavefield, path) -> None:
+    """Write the recorded receiver traces next to a wavefield dump: the fld.it
+    recorded rows (one per step, receivers in config order) as little-endian
+    float32, row-major, with a one-line `n_t n_rec` sidecar at <path>.dims --
+    the trace-file counterpart of `dump_wavefield`."""
+    if fld.traces is None:
+        raise ValidationError("wavefield has no traces (config without receivers)")
+    rows = min(int(fld.it), int(fld.traces.shape[0]))
+    data = np.asarray(fld.traces[:rows].cpu().numpy(), dtype="<f4")
+    with open(path, "wb") as fh:
+        fh.write(data.tobytes(order="C"))
+    with open(f"{path}.dims", "w", encoding="utf-8") as fh:
+        fh.write(f"{data.shape[0]} {data.shape[1]}\n")
+
+
+def load_traces(path) -> np.ndarray:
+    """Read a `dump_traces` file back: (n_t, n_rec) float32."""
+    with open(f"{path}.dims", encoding="utf-8") as fh:
+        shape = tuple(int(v) for v in fh.read().split())
+    if len(shape) != 2:
+        raise ValidationError(f"{path}.dims: expected 'n_t n_rec'")
+    data = np.fromfile(path, dtype="<f4")
+    if data.size != shape[0] * shape[1]:
+        raise ValidationError(f"{path}: {data.size} values, sidecar says {shape}")
+    return data.reshape(shape).astype(np.float32)
+
+
 class HostSimulation:
     """End-to-end simulation from host buffers through `fdr_acoustic_run_host`.
 

@@ -167,3 +167,42 @@ def test_b200_machine_uses_measured_peaks():
     m = roofline.b200_machine()
     assert m.peak_bw_achievable > 5000
     assert m.ridge_point > 5
+
+
+def test_wavefield_and_trace_files_round_trip(tmp_path):
+    import torch
+
+    fld = B.Wavefield(1, [torch.zeros((3, 4, 8)) for _ in range(3)], (3, 4, 5))
+    fld.grids[2][:, :, :5] = torch.arange(60, dtype=torch.float32).reshape(3, 4, 5)
+    fld.traces = torch.arange(12, dtype=torch.float32).reshape(4, 3)
+    fld.it = 3
+    B.dump_wavefield(fld, tmp_path / "u.bin")
+    assert np.array_equal(B.load_wavefield(tmp_path / "u.bin"), fld.numpy(2))
+    B.dump_traces(fld, tmp_path / "t.bin")
+    assert (tmp_path / "t.bin.dims").read_text() == "3 3\n"
+    assert np.array_equal(B.load_traces(tmp_path / "t.bin"), fld.traces[:3].numpy())
+    (tmp_path / "t.bin.dims").write_text("4 4\n")
+    with pytest.raises(B.ValidationError):
+        B.load_traces(tmp_path / "t.bin")
+
+
+def test_oracle_cache_keys_and_reuse(tmp_path, monkeypatch):
+    from oracle import cache
+
+    monkeypatch.setattr(cache, "CACHE_DIR", str(tmp_path))
+    cfg = synthetic.config1(n_t=5)
+    k1 = cache.key("tag", cfg, 5)
+    assert k1 == cache.key("tag", synthetic.config1(n_t=5), 5)
+    assert k1 != cache.key("tag", cfg, 6)
+    m2 = np.array(cfg.m, copy=True)
+    m2[0, 0, 0] *= 2
+    assert k1 != cache.key("tag", B.KernelConfig(order=4, dims=cfg.dims, n_t=5, dt=cfg.dt, h=cfg.h, m=m2), 5)
+    calls = []
+
+    def compute():
+        calls.append(1)
+        return {"a": np.arange(4.0)}
+
+    assert np.array_equal(cache.cached(k1, compute)["a"], np.arange(4.0))
+    assert np.array_equal(cache.cached(k1, compute)["a"], np.arange(4.0))
+    assert len(calls) == 1
