@@ -121,3 +121,18 @@ def test_cli_bench_runs_kernel_and_matches_oracle(cuda_device, tmp_path, capsys)
     cref.simulate(cfg, cfg.n_t, state=st)
     got = np.fromfile(dump, dtype="<f4").reshape(cfg.dims, order="F")
     assert np.array_equal(got, st.latest())
+
+
+def test_artifacts_byte_identical_across_runs(tmp_path):
+    """Acceptance criterion 10 (test_acceptance.py:226-249) for this front end:
+    the SVG and CSV of the same dataset are byte-identical across runs."""
+    m = RL.get_machine("b200")
+    pts = [RL.roofline_point(m, o, measured_gflops=100.0 * o) for o in (2, 8, 16)]
+    outs = []
+    for tag in ("a", "b"):
+        svg, csv = tmp_path / f"r-{tag}.svg", tmp_path / f"r-{tag}.csv"
+        ds = RL.roofline_dataset(m, pts)
+        charts.write_svg(charts.roofline_chart(ds), svg)
+        csv.write_text(ds.to_csv())
+        outs.append((svg.read_bytes(), csv.read_bytes()))
+    assert outs[0] == outs[1] and len(outs[0][0]) > 0 and len(outs[0][1]) > 0
