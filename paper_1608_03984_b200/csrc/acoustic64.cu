@@ -12,13 +12,16 @@
 // parity oracle is oracle/acoustic.py's numpy restatement run on float64
 // levels (tests/test_fp64.py).
 //
-// a64_stream: a 32(z) x 8(y) tile of one point per thread streams along x.
+// a64_queue (AUTO, QUEUE): the TMA-fed register-queue kernel of the float32
+// path, one double2 per thread (below).  a64_stream (variant TMA, kept for
+// comparison): a 32(z) x 8(y) tile of one point per thread streams along x.
 // The 2r+1 x-neighbours of a thread's column live in a register queue; the
 // y/z taps read a shared-memory box of the centre plane (zero halo written
 // explicitly), double-buffered: the box of plane x+1, the queue's next value
 // and this plane's prev / m are loaded into registers before plane x is
 // computed, so their latency overlaps the arithmetic; one barrier per plane.
 // FP64 on B200 is half the FP32 rate and the step is HBM-bound (OI 1.8).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -222,6 +225,313 @@ __global__ void __launch_bounds__(NT, Geo<R>::MINB) a64_stream(const A64Step a) 
   }
 }
 
+// ------------------------------------------------------- TMA queue kernel
+// The float64 counterpart of acoustic_queue (acoustic.cu): 256 threads own a
+// 32(z) x 16(y) tile, one double2 (2 z points) each, and stream it along x.
+// Stage p (filled by TMA NS-1 planes ahead, float64 tensor maps, out-of-bound
+// zero fill = the reference halo) holds the newest plane's tile (register
+// queue along x: 2r+U double2), the centre plane's box with y/z halo, and its
+// prev / m tiles.  Barrier-free recycling: the warp completing a stage's
+// "empty" phase refills it.  Arithmetic in IEEE double, one rounding per op.
+constexpr int QTZ = 32, QTY = 16, QNTZ = QTZ / 2, QNT = QNTZ * QTY;
+
+template <int R>
+struct QG64 {
+  static constexpr int LZ = (R + 1) / 2 * 2;  // z halo in doubles, 16-byte aligned
+  static constexpr int BZ = QTZ + 2 * LZ;
+  static constexpr int BY = QTY + 2 * R;
+  static constexpr int BOX_BYTES = BZ * BY * 8;
+  static constexpr int BOX = (BOX_BYTES + 127) / 128 * 16;  // doubles, 128-B aligned
+  static constexpr int TILE = QTZ * QTY;
+  static constexpr int TILE_BYTES = TILE * 8;
+  static constexpr int OFF_BOX = TILE, OFF_PREV = TILE + BOX, OFF_M = OFF_PREV + TILE;
+  static constexpr int STAGE = OFF_M + TILE;
+  static constexpr int NS = 4;
+  static constexpr int QD = 2 * R + 1;
+  static constexpr int U = R <= 2 ? QD : (R >= 7 ? 1 : 2);
+  static constexpr int NQ = 1 + LZ;  // double2 loads of the own z-row window
+  static constexpr int NWARPS = QNT / 32;
+  static constexpr size_t SMEM = size_t(NS) * STAGE * 8 + 2 * NS * 8;
+};
+
+A64_DEV double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
+A64_DEV void stg2_stream(double* p, double2 v) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+A64_DEV bool arrive_is_last(uint64_t* bar) {
+  uint64_t state;
+  uint32_t pending;
+  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(state) : "r"(fdr::smem_u32(bar)) : "memory");
+  asm volatile("mbarrier.pending_count.b64 %0, %1;" : "=r"(pending) : "l"(state));
+  return pending == 1;
+}
+
+template <bool GRID_M>
+A64_DEV double divide64(const A64Step& a, double s, double m) {
+  if (GRID_M) return __ddiv_rn(s, m);
+  if (a.m_mode == FDR_M_SCALAR) return __ddiv_rn(s, a.m_scalar);
+  return s;
+}
+
+template <int R, bool GRID_M, bool SPONGE>
+__global__ void __launch_bounds__(QNT, 2)
+    a64_queue(const __grid_constant__ CUtensorMap tm_box, const __grid_constant__ CUtensorMap tm_tile,
+              const __grid_constant__ CUtensorMap tm_prev, const __grid_constant__ CUtensorMap tm_m,
+              const A64Step a) {
+  using G = QG64<R>;
+  using namespace fdr;
+  extern __shared__ __align__(128) double dsm[];
+  double* ring = dsm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + G::NS * G::STAGE);
+  uint64_t* empty = full + G::NS;
+
+  gather(a);
+  const int tid = threadIdx.x;
+  const int tz = tid % QNTZ, ty = tid / QNTZ;
+  const int zt = blockIdx.x * QTZ, yt = blockIdx.y * QTY;
+  const int xb = blockIdx.z * a.chunk;
+  const int xe = min(a.nx, xb + a.chunk);
+  if (xb >= xe) return;
+  const int n = xe - xb;
+  const int nplanes = n + 2 * R;  // stream plane p: newest x = xb - R + p
+  const bool leader = (tid & 31) == 0;
+
+  auto issue = [&](int p, int sl) {
+    double* st = ring + sl * G::STAGE;
+    const bool compute = p >= 2 * R;
+    const uint32_t bytes = G::TILE_BYTES + (compute ? G::BOX_BYTES + (GRID_M ? 2 : 1) * G::TILE_BYTES : 0);
+    mbar_arrive_expect_tx(&full[sl], bytes);
+    tma_load_3d(st, &tm_tile, &full[sl], zt, yt, xb - R + p);
+    if (compute) {
+      const int xc = xb - 2 * R + p;
+      tma_load_3d(st + G::OFF_BOX, &tm_box, &full[sl], zt - G::LZ, yt - R, xc);
+      tma_load_3d(st + G::OFF_PREV, &tm_prev, &full[sl], zt, yt, xc);
+      if (GRID_M) tma_load_3d(st + G::OFF_M, &tm_m, &full[sl], zt, yt, xc);
+    }
+  };
+  if (tid == 0) {
+    prefetch_tensormap(&tm_box);
+    prefetch_tensormap(&tm_tile);
+    prefetch_tensormap(&tm_prev);
+    if (GRID_M) prefetch_tensormap(&tm_m);
+    for (int sl = 0; sl < G::NS; ++sl) {
+      mbar_init(&full[sl], 1);
+      mbar_init(&empty[sl], G::NWARPS);
+    }
+    fence_barrier_init();
+    for (int p = 0; p < G::NS && p < nplanes; ++p) issue(p, p);
+  }
+  __syncthreads();
+
+  const int y = yt + ty;
+  const int zb = zt + 2 * tz;
+  const bool row_ok = y < a.ny;
+  const bool vec_ok = row_ok && zb + 1 < a.nz;
+  const int bcen = G::OFF_BOX + (ty + R) * G::BZ + G::LZ + 2 * tz;
+  const int zrow = G::OFF_BOX + (ty + R) * G::BZ + 2 * tz;
+  const int tcol = ty * QTZ + 2 * tz;
+  double gyz0 = 1.0, gyz1 = 1.0, gyv = 1.0;
+  if (SPONGE && row_ok) {
+    gyv = a.gy[y];
+    gyz0 = zb < a.nz ? a.gz[zb] : 1.0;
+    gyz1 = zb + 1 < a.nz ? a.gz[zb + 1] : 1.0;
+  }
+  int src_k = 0, kinj = -1;
+  double qsrc = 0.0;
+  if (a.sx >= 0 && y == a.sy && a.sz >= zb && a.sz < zb + 2 && a.it < a.n_series) {
+    src_k = a.sz - zb;
+    kinj = a.sx - xb;
+    qsrc = a.series[a.it];
+  }
+  double* outp = a.out + (size_t)xb * a.pitch_x + (size_t)y * a.pitch_y + zb;
+
+  int slot = 0;
+  uint32_t phase = 0;
+  auto finish = [&](int p) {
+    __syncwarp();
+    if (leader && arrive_is_last(&empty[slot])) {
+      mbar_wait(&empty[slot], phase);
+      if (p + G::NS < nplanes) issue(p + G::NS, slot);
+    }
+    if (++slot == G::NS) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  };
+
+  constexpr bool ROTATE = G::U % G::QD == 0;
+  double2 qw[2 * R + G::U];
+#pragma unroll
+  for (int p = 0; p < 2 * R; ++p) {
+    mbar_wait(&full[slot], phase);
+    qw[p] = lds2(ring + slot * G::STAGE + tcol);
+    finish(p);
+  }
+
+#pragma unroll 1
+  for (int p0 = 2 * R; p0 < nplanes; p0 += G::U) {
+#pragma unroll
+    for (int u = 0; u < G::U; ++u) {
+      const int p = p0 + u;
+      if (p >= nplanes) break;
+      const int k = p - 2 * R;
+      mbar_wait(&full[slot], phase);
+      const double* st = ring + slot * G::STAGE;
+      qw[ROTATE ? (2 * R + u) % G::QD : 2 * R + u] = lds2(st + tcol);
+      double zr[2 + 2 * G::LZ];
+#pragma unroll
+      for (int qd = 0; qd < G::NQ; ++qd) {
+        const double2 v = lds2(st + zrow + 2 * qd);
+        zr[2 * qd] = v.x;
+        zr[2 * qd + 1] = v.y;
+      }
+      const double c0 = zr[G::LZ], c1 = zr[G::LZ + 1];
+      double l0 = __dmul_rn(a.w[0], c0), l1 = __dmul_rn(a.w[0], c1);
+#pragma unroll
+      for (int j = 1; j <= R; ++j) {  // x taps from the register queue
+        const double2 pp = qw[ROTATE ? (R + u + j) % G::QD : R + u + j];
+        const double2 mm = qw[ROTATE ? (R + u - j + G::QD) % G::QD : R + u - j];
+        l0 = tapd(l0, a.w[j], pp.x, mm.x);
+        l1 = tapd(l1, a.w[j], pp.y, mm.y);
+      }
+#pragma unroll
+      for (int j = 1; j <= R; ++j) {  // y taps from the centre box
+        const double2 pp = lds2(st + bcen + j * G::BZ);
+        const double2 mm = lds2(st + bcen - j * G::BZ);
+        l0 = tapd(l0, a.w[j], pp.x, mm.x);
+        l1 = tapd(l1, a.w[j], pp.y, mm.y);
+      }
+#pragma unroll
+      for (int j = 1; j <= R; ++j) {  // z taps from the own row window
+        l0 = tapd(l0, a.w[j], zr[G::LZ + j], zr[G::LZ - j]);
+        l1 = tapd(l1, a.w[j], zr[G::LZ + 1 + j], zr[G::LZ + 1 - j]);
+      }
+      const double2 pv = lds2(st + G::OFF_PREV + tcol);
+      double2 mv = make_double2(1.0, 1.0);
+      if (GRID_M) mv = lds2(st + G::OFF_M + tcol);
+      finish(p);
+      double o0 = __dadd_rn(__dsub_rn(__dadd_rn(c0, c0), pv.x),
+                            divide64<GRID_M>(a, __dmul_rn(a.coef, l0), mv.x));
+      double o1 = __dadd_rn(__dsub_rn(__dadd_rn(c1, c1), pv.y),
+                            divide64<GRID_M>(a, __dmul_rn(a.coef, l1), mv.y));
+      if (SPONGE) {
+        const double gxy = __dmul_rn(__ldg(a.gx + xb + k), gyv);
+        o0 = __dmul_rn(o0, __dmul_rn(gxy, gyz0));
+        o1 = __dmul_rn(o1, __dmul_rn(gxy, gyz1));
+      }
+      if (k == kinj) {
+        if (src_k == 0) o0 = __dadd_rn(o0, qsrc);
+        else o1 = __dadd_rn(o1, qsrc);
+      }
+      double* dst = outp + (size_t)k * a.pitch_x;
+      if (vec_ok) {
+        stg2_stream(dst, make_double2(o0, o1));
+      } else if (row_ok && zb < a.nz) {
+        dst[0] = o0;
+      }
+    }
+    if (!ROTATE) {
+#pragma unroll
+      for (int i = 0; i < 2 * R; ++i) qw[i] = qw[i + G::U];
+    }
+  }
+}
+
+typedef CUresult (*A64EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+
+static int encode64(CUtensorMap* map, const double* base, const A64Step& s, int box_z, int box_y) {
+  static A64EncodeFn enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(FDR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = reinterpret_cast<A64EncodeFn>(fn);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)s.nz, (cuuint64_t)s.ny, (cuuint64_t)s.nx};
+  cuuint64_t strides[2] = {(cuuint64_t)s.pitch_y * 8, (cuuint64_t)s.pitch_x * 8};
+  cuuint32_t box[3] = {(cuuint32_t)box_z, (cuuint32_t)box_y, 1}, es[3] = {1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? FDR_OK : fail(FDR_ECUDA, "cuTensorMapEncodeTiled (float64) failed (%d)", (int)r);
+}
+
+struct Maps64 {
+  CUtensorMap box[3], tile[3], m;
+};
+
+template <int R, bool GRID_M, bool SPONGE>
+static int queue_inst(const A64Step& s, const Maps64& mp, int k, cudaStream_t st, int* chunk_cache) {
+  using G = QG64<R>;
+  auto kern = a64_queue<R, GRID_M, SPONGE>;
+  static int cfg_dev = -1, occ = 1, nsm = 148;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (cfg_dev != dev) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, QNT, G::SMEM);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "a64_queue setup");
+    if (occ < 1) return fail(FDR_ECUDA, "float64 queue kernel (r=%d) cannot be resident", R);
+    cfg_dev = dev;
+  }
+  const int tzn = (s.nz + QTZ - 1) / QTZ, tyn = (s.ny + QTY - 1) / QTY;
+  if (*chunk_cache <= 0) {
+    const long tiles = (long)tzn * tyn, slots = (long)occ * nsm;
+    double best = 1e30;
+    int best_c = 1;
+    for (int c = 1; c <= std::max(1, s.nx / (2 * R)); ++c) {
+      const int len = (s.nx + c - 1) / c;
+      const int cc = (s.nx + len - 1) / len;
+      const long waves = (tiles * cc + slots - 1) / slots;
+      const double t = (double)waves * (len + 0.3 * 2 * R);
+      if (t < best * 0.999) {
+        best = t;
+        best_c = cc;
+      }
+    }
+    *chunk_cache = (s.nx + best_c - 1) / best_c;
+  }
+  A64Step t = s;
+  t.chunk = *chunk_cache;
+  const int cur = (2 + k) % 3, prev = (1 + k) % 3;
+  dim3 grid(tzn, tyn, (s.nx + t.chunk - 1) / t.chunk);
+  kern<<<grid, QNT, G::SMEM, st>>>(mp.box[cur], mp.tile[cur], mp.tile[prev], mp.m, t);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? FDR_OK : cuda_fail(e, "a64_queue launch");
+}
+
+template <int R>
+static int queue_r(const A64Step& s, const Maps64& mp, int k, cudaStream_t st, int* cc) {
+  const bool gm = s.m_mode == FDR_M_GRID, sp = s.gx != nullptr;
+  if (gm && sp) return queue_inst<R, true, true>(s, mp, k, st, cc);
+  if (gm) return queue_inst<R, true, false>(s, mp, k, st, cc);
+  if (sp) return queue_inst<R, false, true>(s, mp, k, st, cc);
+  return queue_inst<R, false, false>(s, mp, k, st, cc);
+}
+
+static int queue_step(const A64Step& s, const Maps64& mp, int k, cudaStream_t st, int* cc) {
+  switch (s.radius) {
+    case 1: return queue_r<1>(s, mp, k, st, cc);
+    case 2: return queue_r<2>(s, mp, k, st, cc);
+    case 3: return queue_r<3>(s, mp, k, st, cc);
+    case 4: return queue_r<4>(s, mp, k, st, cc);
+    case 5: return queue_r<5>(s, mp, k, st, cc);
+    case 6: return queue_r<6>(s, mp, k, st, cc);
+    case 7: return queue_r<7>(s, mp, k, st, cc);
+    case 8: return queue_r<8>(s, mp, k, st, cc);
+    default: return fail(FDR_EINVAL, "float64 queue kernel supports radius <= 8, got %d", s.radius);
+  }
+}
+
 template <int R>
 static int stream_launch(const A64Step& s, cudaStream_t st, int* chunk_cache) {
   using G = Geo<R>;
@@ -306,11 +616,14 @@ static int validate(const fdr_acoustic64_args* a) {
     return fail(FDR_EINVAL, "source series pointer NULL");
   if (a->n_rec < 0 || (a->n_rec > 0 && (!a->rec_xyz || !a->traces)))
     return fail(FDR_EINVAL, "receiver coordinates or trace buffer NULL");
-  if (a->variant != FDR_VARIANT_AUTO && a->variant != FDR_VARIANT_DIRECT &&
-      a->variant != FDR_VARIANT_QUEUE)
-    return fail(FDR_EINVAL, "fp64 variant must be AUTO, DIRECT or QUEUE, got %d", a->variant);
-  if (a->variant == FDR_VARIANT_QUEUE && r > 8)
-    return fail(FDR_EINVAL, "fp64 streaming kernel supports order <= 16, got %d", a->order);
+  if (a->variant < FDR_VARIANT_AUTO || a->variant > FDR_VARIANT_QUEUE)
+    return fail(FDR_EINVAL, "fp64 variant must be AUTO, DIRECT, TMA or QUEUE, got %d", a->variant);
+  if ((a->variant == FDR_VARIANT_QUEUE || a->variant == FDR_VARIANT_TMA) && r > 8)
+    return fail(FDR_EINVAL, "fp64 streaming kernels support order <= 16, got %d", a->order);
+  if (a->variant != FDR_VARIANT_DIRECT &&
+      ((uintptr_t)a->levels[0] % 16 || (uintptr_t)a->levels[1] % 16 || (uintptr_t)a->levels[2] % 16 ||
+       (a->m_mode == FDR_M_GRID && (uintptr_t)a->m % 16)))
+    return fail(FDR_EINVAL, "fp64 streaming kernels need 16-byte aligned levels and m");
   return FDR_OK;
 }
 
@@ -348,12 +661,29 @@ static void fill(A64Step& s, const fdr_acoustic64_args* a, int k) {
 
 static int run(const fdr_acoustic64_args* a, cudaStream_t st) {
   const int r = a->order / 2;
-  const bool stream = a->variant == FDR_VARIANT_QUEUE || (a->variant == FDR_VARIANT_AUTO && r <= 8);
+  const bool queue = a->variant == FDR_VARIANT_QUEUE || (a->variant == FDR_VARIANT_AUTO && r <= 8);
+  const bool stream = a->variant == FDR_VARIANT_TMA;  // plain-load streaming kernel
+  Maps64 mp;
+  if (queue && a->n_steps > 0) {
+    A64Step s0;
+    fill(s0, a, 0);
+    const int lz = (r + 1) / 2 * 2;
+    for (int i = 0; i < 3; ++i) {
+      int rc = encode64(&mp.box[i], a->levels[i], s0, QTZ + 2 * lz, QTY + 2 * r);
+      if (rc == FDR_OK) rc = encode64(&mp.tile[i], a->levels[i], s0, QTZ, QTY);
+      if (rc != FDR_OK) return rc;
+    }
+    const int rc = encode64(&mp.m, a->m_mode == FDR_M_GRID ? a->m : a->levels[0], s0, QTZ, QTY);
+    if (rc != FDR_OK) return rc;
+  }
   int chunk = 0;
   for (int k = 0; k < a->n_steps; ++k) {
     A64Step s;
     fill(s, a, k);
-    if (stream) {
+    if (queue) {
+      const int rc = queue_step(s, mp, k, st, &chunk);
+      if (rc != FDR_OK) return rc;
+    } else if (stream) {
       const int rc = stream_step(s, st, &chunk);
       if (rc != FDR_OK) return rc;
     } else {

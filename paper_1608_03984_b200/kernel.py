@@ -461,8 +461,8 @@ def _run_f64(fld: Wavefield, cfg: KernelConfig, n: int, variant: str) -> Wavefie
     torch = _torch()
     lib = _lib.load()
     dev = fld.device
-    if variant == "tma":
-        raise ValidationError("the float64 path has variants auto, queue and direct")
+    if variant == "persistent":
+        raise ValidationError("the float64 path has variants auto, queue, tma and direct")
     pitch_y = int(fld.grids[0].shape[2])
     pitch_x = int(fld.grids[0].shape[1]) * pitch_y
     plan = getattr(cfg, "_device_plan64", None)

@@ -98,7 +98,7 @@ CASES = {
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", ["queue", "direct"])
+@pytest.mark.parametrize("variant", ["queue", "tma", "direct"])
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_gpu_f64_bitexact_vs_oracle(B, case, variant):
     cfg, levels = CASES[case]()
@@ -142,20 +142,22 @@ def test_gpu_f64_config1_sponge_source_receivers(B):
 
 @pytest.mark.gpu
 def test_gpu_f64_stream_equals_direct_medium(B):
-    """96x80x72 order 8 with every extension, 40 steps: streaming == direct."""
+    """96x80x72 order 8 with every extension, 40 steps: both streaming
+    kernels == direct."""
     cfg, _ = medium_o8_case()
-    a = _gpu_f64(B, cfg, None, "queue")
     b = _gpu_f64(B, cfg, None, "direct")
-    assert sha64(a.numpy()) == sha64(b.numpy())
-    assert sha64(a.traces.cpu().numpy()) == sha64(b.traces.cpu().numpy())
-    assert np.abs(a.numpy()).max() > 0
+    for v in ("queue", "tma"):
+        a = _gpu_f64(B, cfg, None, v)
+        assert sha64(a.numpy()) == sha64(b.numpy()), v
+        assert sha64(a.traces.cpu().numpy()) == sha64(b.traces.cpu().numpy()), v
+    assert np.abs(b.numpy()).max() > 0
 
 
 @pytest.mark.gpu
-def test_gpu_f64_rejects_tma_variant(B):
+def test_gpu_f64_rejects_persistent_variant(B):
     import torch
 
     cfg, levels = random_case(4)
     fld = B.Wavefield.allocate(cfg.dims, cfg.halo, dtype=torch.float64)
     with pytest.raises(B.ValidationError):
-        B.run(fld, cfg, variant="tma")
+        B.run(fld, cfg, variant="persistent")

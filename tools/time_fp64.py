@@ -29,7 +29,7 @@ def main():
         nz = dims[2]
         for g in fld.grids:
             g[:, :, nz:] = 0
-        for variant in ("queue", "direct") if order <= 8 else ("queue",):
+        for variant in ("queue", "tma", "direct") if order <= 8 else ("queue", "tma"):
             B.run(fld, cfg, 2, variant=variant)
             torch.cuda.synchronize()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
