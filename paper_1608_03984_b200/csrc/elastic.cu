@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(256) el_str_direct(const ElStep a) {
   } while (0)
 
 int el_stream_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, int* chunk_cache);
+int el_queue_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, int* chunk_cache);
 
 static int validate(const fdr_elastic_args* a) {
   if (!a) return fail(FDR_EINVAL, "args is NULL");
@@ -182,7 +183,7 @@ static int validate(const fdr_elastic_args* a) {
     return fail(FDR_EINVAL, "source location outside interior");
   if (a->n_rec > 0 && (!a->rec_xyz || !a->traces))
     return fail(FDR_EINVAL, "receiver coordinates or trace buffer NULL");
-  if (a->variant < 0 || a->variant > FDR_VARIANT_QUEUE || a->variant == FDR_VARIANT_TMA)
+  if (a->variant < 0 || a->variant > FDR_VARIANT_QUEUE)
     return fail(FDR_EINVAL, "unknown elastic variant %d", a->variant);
   return FDR_OK;
 }
@@ -222,13 +223,16 @@ static int run(const fdr_elastic_args* a, cudaStream_t st) {
   const bool small_index = (uint64_t)a->nx * (uint64_t)a->pitch_x < (1ull << 32);
   if (variant == FDR_VARIANT_AUTO)
     variant = (a->order <= 8 && small_index) ? FDR_VARIANT_QUEUE : FDR_VARIANT_DIRECT;
-  if (variant == FDR_VARIANT_QUEUE && (!small_index || a->order > 8))
-    return fail(FDR_EINVAL, "the elastic stream kernel needs order <= 8 and < 2^32 elements");
+  if ((variant == FDR_VARIANT_QUEUE || variant == FDR_VARIANT_TMA) && (!small_index || a->order > 8))
+    return fail(FDR_EINVAL, "the elastic streaming kernels need order <= 8 and < 2^32 elements");
   int chunk = 0;
   for (int k = 0; k < a->n_steps; ++k) {
     ElStep s;
     fill(s, a, k);
-    if (variant == FDR_VARIANT_QUEUE) {
+    if (variant == FDR_VARIANT_QUEUE) {  // el_queue (production)
+      int rc = el_queue_step(s, a, st, &chunk);
+      if (rc != FDR_OK) return rc;
+    } else if (variant == FDR_VARIANT_TMA) {  // el_stream (previous design)
       int rc = el_stream_step(s, a, st, &chunk);
       if (rc != FDR_OK) return rc;
     } else {
@@ -538,6 +542,413 @@ static int el_encode(CUtensorMap* map, const float* base, const fdr_elastic_args
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FDR_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return FDR_OK;
+}
+
+// ======================================================= queue kernels
+// el_queue<R, PASS, SPONGE>: the acoustic_queue design for the two elastic
+// passes.  256 threads own a 32(z) x 16(y) tile, one float2 (2 z points) each,
+// and stream it along x.  Stage p (TMA, NS-1 planes ahead) holds
+//   - the newest plane's tiles of the three fields differentiated along x
+//     (velocity pass: sxx sxy sxz; stress pass: vx vy vz), appended to
+//     per-thread register queues of 2r+U float2;
+//   - the centre plane's (x = newest - r) boxes, each with only the halo its
+//     in-plane derivatives need (y-only, z-only or both), and its tiles.
+// All in-plane derivatives are formed from the centre boxes when the centre
+// plane is computed, so nothing is carried across planes but the x queues.
+// Same float32 sequence as el_stream / oracle/elastic_ref.c.
+constexpr int QZ = 32, QY = 16, QNZ = QZ / 2, QN = QNZ * QY;
+
+template <int R, int PASS>
+struct QGeoE {
+  // z halo in floats: the TMA box must start on a 16-byte boundary (a 2-float
+  // halo, i.e. an 8-byte offset, faults with an illegal instruction)
+  static constexpr int LZ = (R + 3) / 4 * 4;
+  static constexpr int ZB = QZ + 2 * LZ, YB = QY + 2 * R;    // boxed extents
+  static constexpr int TILE = QZ * QY;
+  static constexpr int al(int f) { return (f + 31) / 32 * 32; }  // 128-byte aligned regions
+  static constexpr int YBOX = al(QZ * YB), ZBOX = al(ZB * QY), FBOX = al(ZB * YB);
+  static constexpr int NY = PASS == 0 ? 2 : 0, NZB = PASS == 0 ? 2 : 0, NF = PASS == 0 ? 1 : 3;
+  static constexpr int NC = PASS == 0 ? 4 : 8;               // centre tiles
+  static constexpr int O_WIN = 0;
+  static constexpr int O_Y = 3 * TILE;
+  static constexpr int O_Z = O_Y + NY * YBOX;
+  static constexpr int O_F = O_Z + NZB * ZBOX;
+  static constexpr int O_C = O_F + NF * FBOX;
+  static constexpr int STAGE = O_C + NC * TILE;
+  static constexpr int NS = 3;
+  static constexpr int QD = 2 * R + 1;
+  static constexpr int U = R <= 2 ? QD : 2;
+  static constexpr int NWARPS = QN / 32;
+  static constexpr size_t SMEM = size_t(NS) * STAGE * 4 + 2 * NS * 8;
+  static constexpr uint32_t WIN_BYTES = 3 * TILE * 4;
+  static constexpr uint32_t CEN_BYTES = (NY * QZ * YB + NZB * ZB * QY + NF * ZB * YB + NC * TILE) * 4;
+};
+
+struct ElQMaps {
+  CUtensorMap win[3];   // newest-plane tiles of the x-differentiated fields
+  CUtensorMap ybox[2];  // velocity pass: sxy syy
+  CUtensorMap zbox[2];  // velocity pass: sxz szz
+  CUtensorMap fbox[3];  // velocity pass: syz; stress pass: vx vy vz
+  CUtensorMap ctile[8]; // velocity: vx vy vz bs; stress: sxx syy szz sxy sxz syz lam mu
+};
+
+// staggered differences for the two lanes of a float2 column: p points at the
+// own pair, s = the element stride of the differenced axis (multiple of 2)
+template <int R>
+FDR_DEV float2 pF2(const float* p, int s, const float* c) {
+  float2 a = *reinterpret_cast<const float2*>(p + s), b = *reinterpret_cast<const float2*>(p);
+  float2 d = make_float2(__fmul_rn(c[1], __fsub_rn(a.x, b.x)), __fmul_rn(c[1], __fsub_rn(a.y, b.y)));
+#pragma unroll
+  for (int k = 2; k <= R; ++k) {
+    a = *reinterpret_cast<const float2*>(p + k * s);
+    b = *reinterpret_cast<const float2*>(p + (1 - k) * s);
+    d = make_float2(__fmaf_rn(c[k], __fsub_rn(a.x, b.x), d.x), __fmaf_rn(c[k], __fsub_rn(a.y, b.y), d.y));
+  }
+  return d;
+}
+template <int R>
+FDR_DEV float2 pB2(const float* p, int s, const float* c) {
+  float2 a = *reinterpret_cast<const float2*>(p), b = *reinterpret_cast<const float2*>(p - s);
+  float2 d = make_float2(__fmul_rn(c[1], __fsub_rn(a.x, b.x)), __fmul_rn(c[1], __fsub_rn(a.y, b.y)));
+#pragma unroll
+  for (int k = 2; k <= R; ++k) {
+    a = *reinterpret_cast<const float2*>(p + (k - 1) * s);
+    b = *reinterpret_cast<const float2*>(p - k * s);
+    d = make_float2(__fmaf_rn(c[k], __fsub_rn(a.x, b.x), d.x), __fmaf_rn(c[k], __fsub_rn(a.y, b.y), d.y));
+  }
+  return d;
+}
+// along z within one row window w[] (w[LZ] = the own pair's first point)
+template <int R, int LZ>
+FDR_DEV float2 zF2(const float* w, const float* c) {
+  float2 d;
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    const int i = LZ + l;
+    float v = __fmul_rn(c[1], __fsub_rn(w[i + 1], w[i]));
+#pragma unroll
+    for (int k = 2; k <= R; ++k) v = __fmaf_rn(c[k], __fsub_rn(w[i + k], w[i + 1 - k]), v);
+    (l == 0 ? d.x : d.y) = v;
+  }
+  return d;
+}
+template <int R, int LZ>
+FDR_DEV float2 zB2(const float* w, const float* c) {
+  float2 d;
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    const int i = LZ + l;
+    float v = __fmul_rn(c[1], __fsub_rn(w[i], w[i - 1]));
+#pragma unroll
+    for (int k = 2; k <= R; ++k) v = __fmaf_rn(c[k], __fsub_rn(w[i + k - 1], w[i - k]), v);
+    (l == 0 ? d.x : d.y) = v;
+  }
+  return d;
+}
+// along x from a register queue of float2 (centre index cidx)
+template <int R, int QD, bool ROT>
+FDR_DEV float2 xF2(const float2* q, int cidx, const float* c) {
+  auto at = [&](int i) -> float2 { return q[ROT ? (i + QD) % QD : i]; };
+  float2 a = at(cidx + 1), b = at(cidx);
+  float2 d = make_float2(__fmul_rn(c[1], __fsub_rn(a.x, b.x)), __fmul_rn(c[1], __fsub_rn(a.y, b.y)));
+#pragma unroll
+  for (int k = 2; k <= R; ++k) {
+    a = at(cidx + k);
+    b = at(cidx + 1 - k);
+    d = make_float2(__fmaf_rn(c[k], __fsub_rn(a.x, b.x), d.x), __fmaf_rn(c[k], __fsub_rn(a.y, b.y), d.y));
+  }
+  return d;
+}
+template <int R, int QD, bool ROT>
+FDR_DEV float2 xB2(const float2* q, int cidx, const float* c) {
+  auto at = [&](int i) -> float2 { return q[ROT ? (i + QD) % QD : i]; };
+  float2 a = at(cidx), b = at(cidx - 1);
+  float2 d = make_float2(__fmul_rn(c[1], __fsub_rn(a.x, b.x)), __fmul_rn(c[1], __fsub_rn(a.y, b.y)));
+#pragma unroll
+  for (int k = 2; k <= R; ++k) {
+    a = at(cidx + k - 1);
+    b = at(cidx - k);
+    d = make_float2(__fmaf_rn(c[k], __fsub_rn(a.x, b.x), d.x), __fmaf_rn(c[k], __fsub_rn(a.y, b.y), d.y));
+  }
+  return d;
+}
+FDR_DEV float2 add2f(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
+FDR_DEV float2 fma2f(float2 a, float2 b, float2 c) {
+  return make_float2(__fmaf_rn(a.x, b.x, c.x), __fmaf_rn(a.y, b.y, c.y));
+}
+FDR_DEV void stg2cs(float* p, float2 v) {
+  asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+
+template <int R, int PASS, bool SPONGE>
+__global__ void __launch_bounds__(QN, 2) el_queue(const __grid_constant__ ElQMaps maps, const ElStep a) {
+  using G = QGeoE<R, PASS>;
+  constexpr int LZ = G::LZ;
+  extern __shared__ __align__(128) float smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::NS * G::STAGE);
+  uint64_t* empty = full + G::NS;
+  if (PASS == 1) gather_vz(a);
+  const int tid = threadIdx.x;
+  const int tz = tid % QNZ, ty = tid / QNZ;
+  const int zt = blockIdx.x * QZ, yt = blockIdx.y * QY;
+  const int xb = blockIdx.z * a.chunk;
+  const int xe = min(a.nx, xb + a.chunk);
+  if (xb >= xe) return;
+  const int n = xe - xb;
+  const int nplanes = n + 2 * R;
+  const bool leader = (tid & 31) == 0;
+
+  auto issue = [&](int pl, int sl) {
+    float* st = smem + sl * G::STAGE;
+    const int xn = xb - R + pl;
+    const bool cen = pl >= 2 * R;
+    mbar_arrive_expect_tx(&full[sl], G::WIN_BYTES + (cen ? G::CEN_BYTES : 0));
+#pragma unroll
+    for (int f = 0; f < 3; ++f) tma_load_3d(st + G::O_WIN + f * G::TILE, &maps.win[f], &full[sl], zt, yt, xn);
+    if (cen) {
+      const int xc = xn - R;
+#pragma unroll
+      for (int b = 0; b < G::NY; ++b) tma_load_3d(st + G::O_Y + b * G::YBOX, &maps.ybox[b], &full[sl], zt, yt - R, xc);
+#pragma unroll
+      for (int b = 0; b < G::NZB; ++b) tma_load_3d(st + G::O_Z + b * G::ZBOX, &maps.zbox[b], &full[sl], zt - LZ, yt, xc);
+#pragma unroll
+      for (int b = 0; b < G::NF; ++b) tma_load_3d(st + G::O_F + b * G::FBOX, &maps.fbox[b], &full[sl], zt - LZ, yt - R, xc);
+#pragma unroll
+      for (int t = 0; t < G::NC; ++t) tma_load_3d(st + G::O_C + t * G::TILE, &maps.ctile[t], &full[sl], zt, yt, xc);
+    }
+  };
+  if (tid == 0) {
+    for (int f = 0; f < 3; ++f) prefetch_tensormap(&maps.win[f]);
+    for (int sl = 0; sl < G::NS; ++sl) {
+      mbar_init(&full[sl], 1);
+      mbar_init(&empty[sl], G::NWARPS);
+    }
+    fence_barrier_init();
+    for (int pl = 0; pl < G::NS && pl < nplanes; ++pl) issue(pl, pl);
+  }
+  __syncthreads();
+
+  const int y = yt + ty, zb = zt + 2 * tz;
+  const bool row_ok = y < a.ny;
+  const bool vec_ok = row_ok && zb + 1 < a.nz;
+  const int tcol = ty * QZ + 2 * tz;                    // own pair in a tile
+  const int ycol = (ty + R) * QZ + 2 * tz;              // in a y-box
+  const int zrow = ty * G::ZB + 2 * tz;                 // own row window start in a z-box
+  const int frow = (ty + R) * G::ZB + 2 * tz;           // own row window start in a full box
+  float gy = 1.0f, gz0 = 1.0f, gz1 = 1.0f;
+  if (SPONGE && row_ok) {
+    gy = a.gy[y];
+    gz0 = zb < a.nz ? a.gz[zb] : 1.0f;
+    gz1 = zb + 1 < a.nz ? a.gz[zb + 1] : 1.0f;
+  }
+  int kinj = -1, src_l = 0;
+  float qsrc = 0.0f;
+  if (PASS == 1 && a.sx >= 0 && y == a.sy && a.sz >= zb && a.sz < zb + 2 && a.it < a.n_series) {
+    kinj = a.sx - xb;
+    src_l = a.sz - zb;
+    qsrc = a.series[a.it];
+  }
+  const size_t obase = (size_t)xb * a.pitch_x + (size_t)y * a.pitch_y + zb;
+
+  int slot = 0;
+  uint32_t phase = 0;
+  constexpr bool ROT = G::U % G::QD == 0;
+  float2 q0[2 * R + G::U], q1[2 * R + G::U], q2[2 * R + G::U];
+
+#pragma unroll 1
+  for (int p0 = 0; p0 < nplanes; p0 += G::U) {
+#pragma unroll
+    for (int u = 0; u < G::U; ++u) {
+      const int pl = p0 + u;
+      if (pl >= nplanes) break;
+      mbar_wait(&full[slot], phase);
+      const float* st = smem + slot * G::STAGE;
+      // queue slot of the newest plane: index 2R + u of this round (plane p0 - 2R + i at i)
+      const int qn = ROT ? (2 * R + u) % G::QD : 2 * R + u;
+      q0[qn] = *reinterpret_cast<const float2*>(st + G::O_WIN + tcol);
+      q1[qn] = *reinterpret_cast<const float2*>(st + G::O_WIN + G::TILE + tcol);
+      q2[qn] = *reinterpret_cast<const float2*>(st + G::O_WIN + 2 * G::TILE + tcol);
+      const int k = pl - 2 * R;
+      float2 out[6];
+      if (k >= 0) {
+        const int ci = R + u;  // queue index of the centre plane
+        if (PASS == 0) {
+          const float* sxy = st + G::O_Y + ycol;
+          const float* syy = st + G::O_Y + G::YBOX + ycol;
+          float zw[2 + 2 * LZ], zw2[2 + 2 * LZ], fw[2 + 2 * LZ];
+#pragma unroll
+          for (int i = 0; i < 1 + LZ; ++i) {
+            const float2 v = *reinterpret_cast<const float2*>(st + G::O_Z + zrow + 2 * i);
+            const float2 w = *reinterpret_cast<const float2*>(st + G::O_Z + G::ZBOX + zrow + 2 * i);
+            const float2 f = *reinterpret_cast<const float2*>(st + G::O_F + frow + 2 * i);
+            zw[2 * i] = v.x; zw[2 * i + 1] = v.y;
+            zw2[2 * i] = w.x; zw2[2 * i + 1] = w.y;
+            fw[2 * i] = f.x; fw[2 * i + 1] = f.y;
+          }
+          const float* syz = st + G::O_F + frow + LZ;
+          const float2 d0 = add2f(pB2<R>(sxy, QZ, a.c), zB2<R, LZ>(zw, a.c));     // By sxy + Bz sxz
+          const float2 d1 = add2f(pF2<R>(syy, QZ, a.c), zB2<R, LZ>(fw, a.c));     // Fy syy + Bz syz
+          const float2 d2 = add2f(pB2<R>(syz, G::ZB, a.c), zF2<R, LZ>(zw2, a.c)); // By syz + Fz szz
+          const float* ct = st + G::O_C + tcol;
+          const float2 vx = *reinterpret_cast<const float2*>(ct);
+          const float2 vy = *reinterpret_cast<const float2*>(ct + G::TILE);
+          const float2 vz = *reinterpret_cast<const float2*>(ct + 2 * G::TILE);
+          const float2 bs = *reinterpret_cast<const float2*>(ct + 3 * G::TILE);
+          out[0] = fma2f(bs, add2f(d0, xF2<R, G::QD, ROT>(q0, ci, a.c)), vx);
+          out[1] = fma2f(bs, add2f(d1, xB2<R, G::QD, ROT>(q1, ci, a.c)), vy);
+          out[2] = fma2f(bs, add2f(d2, xB2<R, G::QD, ROT>(q2, ci, a.c)), vz);
+        } else {
+          float xw[2 + 2 * LZ], yw[2 + 2 * LZ], zw[2 + 2 * LZ];
+#pragma unroll
+          for (int i = 0; i < 1 + LZ; ++i) {
+            const float2 v0 = *reinterpret_cast<const float2*>(st + G::O_F + frow + 2 * i);
+            const float2 v1 = *reinterpret_cast<const float2*>(st + G::O_F + G::FBOX + frow + 2 * i);
+            const float2 v2 = *reinterpret_cast<const float2*>(st + G::O_F + 2 * G::FBOX + frow + 2 * i);
+            xw[2 * i] = v0.x; xw[2 * i + 1] = v0.y;
+            yw[2 * i] = v1.x; yw[2 * i + 1] = v1.y;
+            zw[2 * i] = v2.x; zw[2 * i + 1] = v2.y;
+          }
+          const float* vxb = st + G::O_F + frow + LZ;
+          const float* vyb = vxb + G::FBOX;
+          const float* vzb = vxb + 2 * G::FBOX;
+          const float2 ey = pB2<R>(vyb, G::ZB, a.c);
+          const float2 ez = zB2<R, LZ>(zw, a.c);
+          const float2 fyvx = pF2<R>(vxb, G::ZB, a.c);
+          const float2 fzvx = zF2<R, LZ>(xw, a.c);
+          const float2 d4 = add2f(zF2<R, LZ>(yw, a.c), pF2<R>(vzb, G::ZB, a.c));  // Fz vy + Fy vz
+          const float2 ex = xB2<R, G::QD, ROT>(q0, ci, a.c);
+          const float* ct = st + G::O_C + tcol;
+          float2 cv[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) cv[t] = *reinterpret_cast<const float2*>(ct + t * G::TILE);
+          const float2 lam = cv[6], mu = cv[7];
+          const float2 l2m = make_float2(__fmaf_rn(2.0f, mu.x, lam.x), __fmaf_rn(2.0f, mu.y, lam.y));
+          out[0] = fma2f(lam, add2f(ey, ez), fma2f(l2m, ex, cv[0]));
+          out[1] = fma2f(lam, add2f(ez, ex), fma2f(l2m, ey, cv[1]));
+          out[2] = fma2f(lam, add2f(ey, ex), fma2f(l2m, ez, cv[2]));
+          out[3] = fma2f(mu, add2f(fyvx, xF2<R, G::QD, ROT>(q1, ci, a.c)), cv[3]);
+          out[4] = fma2f(mu, add2f(fzvx, xF2<R, G::QD, ROT>(q2, ci, a.c)), cv[4]);
+          out[5] = fma2f(mu, d4, cv[5]);
+        }
+      }
+      // release the stage (every read of it is above)
+      __syncwarp();
+      if (leader && el_arrive_last(&empty[slot])) {
+        mbar_wait(&empty[slot], phase);
+        if (pl + G::NS < nplanes) issue(pl + G::NS, slot);
+      }
+      if (++slot == G::NS) {
+        slot = 0;
+        phase ^= 1u;
+      }
+      if (k >= 0) {
+        constexpr int NO = PASS == 0 ? 3 : 6;
+        if (SPONGE) {
+          const float gxy = __fmul_rn(__ldg(a.gx + xb + k), gy);
+          const float g0 = __fmul_rn(gxy, gz0), g1 = __fmul_rn(gxy, gz1);
+#pragma unroll
+          for (int i = 0; i < NO; ++i) out[i] = make_float2(__fmul_rn(out[i].x, g0), __fmul_rn(out[i].y, g1));
+        }
+        if (PASS == 1 && k == kinj) {
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            if (src_l == 0) out[i].x = __fadd_rn(out[i].x, qsrc);
+            else out[i].y = __fadd_rn(out[i].y, qsrc);
+          }
+        }
+        const size_t o = obase + (size_t)k * a.pitch_x;
+#pragma unroll
+        for (int i = 0; i < NO; ++i) {
+          float* dst = a.f[(PASS == 0 ? VX : SXX) + i] + o;
+          if (vec_ok) stg2cs(dst, out[i]);
+          else if (row_ok && zb < a.nz) dst[0] = out[i].x;
+        }
+      }
+    }
+    if (!ROT) {
+#pragma unroll
+      for (int i = 0; i < 2 * R; ++i) {
+        q0[i] = q0[i + G::U];
+        q1[i] = q1[i + G::U];
+        q2[i] = q2[i + G::U];
+      }
+    }
+  }
+}
+
+template <int R, int PASS>
+static int elq_launch(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, int* chunk_cache) {
+  using G = QGeoE<R, PASS>;
+  const bool sponge = s.gx != nullptr;
+  auto kern = sponge ? el_queue<R, PASS, true> : el_queue<R, PASS, false>;
+  static int configured[2] = {-1, -1}, occ[2] = {1, 1};
+  int dev = 0;
+  EL_CUDA(cudaGetDevice(&dev));
+  if (configured[sponge] != dev) {
+    EL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    EL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[sponge], kern, QN, G::SMEM));
+    if (occ[sponge] < 1) return fail(FDR_ECUDA, "elastic queue kernel (r=%d) cannot be resident", R);
+    configured[sponge] = dev;
+  }
+  const int tzn = (a->nz + QZ - 1) / QZ, tyn = (a->ny + QY - 1) / QY;
+  if (*chunk_cache <= 0) {
+    int nsm = 148;
+    EL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const long tiles = (long)tzn * tyn, slots = (long)nsm * occ[sponge];
+    double best = 1e30;
+    int best_c = 1;
+    for (int c = 1; c <= std::max(1, a->nx / (2 * R)); ++c) {
+      const int len = (a->nx + c - 1) / c;
+      const int cc = (a->nx + len - 1) / len;
+      const long waves = (tiles * cc + slots - 1) / slots;
+      const double tt = (double)waves * (len + 0.3 * 2 * R);
+      if (tt < best * 0.999) {
+        best = tt;
+        best_c = cc;
+      }
+    }
+    *chunk_cache = (a->nx + best_c - 1) / best_c;
+  }
+  ElQMaps maps;
+  int rc = FDR_OK;
+  const int ZBW = QZ + 2 * G::LZ, YBH = QY + 2 * R;
+  if (PASS == 0) {
+    const int win[3] = {SXX, SXY, SXZ};
+    for (int f = 0; f < 3 && rc == FDR_OK; ++f) rc = el_encode(&maps.win[f], a->fields[win[f]], a, QZ, QY);
+    if (rc == FDR_OK) rc = el_encode(&maps.ybox[0], a->fields[SXY], a, QZ, YBH);
+    if (rc == FDR_OK) rc = el_encode(&maps.ybox[1], a->fields[SYY], a, QZ, YBH);
+    if (rc == FDR_OK) rc = el_encode(&maps.zbox[0], a->fields[SXZ], a, ZBW, QY);
+    if (rc == FDR_OK) rc = el_encode(&maps.zbox[1], a->fields[SZZ], a, ZBW, QY);
+    if (rc == FDR_OK) rc = el_encode(&maps.fbox[0], a->fields[SYZ], a, ZBW, YBH);
+    const float* ct[4] = {a->fields[VX], a->fields[VY], a->fields[VZ], a->params[0]};
+    for (int t = 0; t < 4 && rc == FDR_OK; ++t) rc = el_encode(&maps.ctile[t], ct[t], a, QZ, QY);
+  } else {
+    const int win[3] = {VX, VY, VZ};
+    for (int f = 0; f < 3 && rc == FDR_OK; ++f) rc = el_encode(&maps.win[f], a->fields[win[f]], a, QZ, QY);
+    for (int f = 0; f < 3 && rc == FDR_OK; ++f) rc = el_encode(&maps.fbox[f], a->fields[win[f]], a, ZBW, YBH);
+    const float* ct[8] = {a->fields[SXX], a->fields[SYY], a->fields[SZZ], a->fields[SXY],
+                          a->fields[SXZ], a->fields[SYZ], a->params[1], a->params[2]};
+    for (int t = 0; t < 8 && rc == FDR_OK; ++t) rc = el_encode(&maps.ctile[t], ct[t], a, QZ, QY);
+  }
+  if (rc != FDR_OK) return rc;
+  ElStep t = s;
+  t.chunk = *chunk_cache;
+  dim3 grid(tzn, tyn, (a->nx + t.chunk - 1) / t.chunk);
+  kern<<<grid, QN, G::SMEM, st>>>(maps, t);
+  EL_CUDA(cudaGetLastError());
+  return FDR_OK;
+}
+
+int el_queue_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, int* chunk_cache) {
+  int rc = FDR_OK;
+  switch (a->order / 2) {
+    case 1: rc = elq_launch<1, 0>(s, a, st, chunk_cache); if (rc == FDR_OK) rc = elq_launch<1, 1>(s, a, st, chunk_cache); break;
+    case 2: rc = elq_launch<2, 0>(s, a, st, chunk_cache); if (rc == FDR_OK) rc = elq_launch<2, 1>(s, a, st, chunk_cache); break;
+    case 3: rc = elq_launch<3, 0>(s, a, st, chunk_cache); if (rc == FDR_OK) rc = elq_launch<3, 1>(s, a, st, chunk_cache); break;
+    case 4: rc = elq_launch<4, 0>(s, a, st, chunk_cache); if (rc == FDR_OK) rc = elq_launch<4, 1>(s, a, st, chunk_cache); break;
+    default: return fail(FDR_EINVAL, "elastic queue kernel supports orders 2..8, got %d", a->order);
+  }
+  return rc;
 }
 
 template <int R, int PASS>

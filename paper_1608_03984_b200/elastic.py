@@ -207,7 +207,7 @@ def _el_key(cfg, device):
             id(cfg.rho), id(cfg.source), id(cfg.receivers), id(cfg.sponge), str(device))
 
 
-_VARIANTS = {"auto": 0, "direct": 1, "stream": 3}
+_VARIANTS = {"auto": 0, "direct": 1, "stream": 2, "queue": 3}
 
 
 def elastic_run(fld: ElasticWavefield, cfg: ElasticConfig, n_steps: Optional[int] = None,

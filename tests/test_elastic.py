@@ -84,7 +84,7 @@ def el_mod(cuda_device):
     return elastic
 
 
-GPU_VARIANTS = ["stream", "direct"]
+GPU_VARIANTS = ["queue", "stream", "direct"]
 
 
 @pytest.mark.gpu

@@ -16,7 +16,7 @@ def main():
     nt = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     cfg = elastic.config5(n_t=nt)
     npts = float(np.prod(cfg.dims))
-    for variant in ("stream",):
+    for variant in ("queue", "stream"):
         fld = elastic.ElasticWavefield.allocate(cfg.dims, cfg.halo)
         elastic.elastic_run(fld, cfg, 2, variant=variant)
         torch.cuda.synchronize()
