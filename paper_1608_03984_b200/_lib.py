@@ -131,6 +131,9 @@ EXPORTS = (
     ("fdr_elastic_run", ctypes.c_int, (ctypes.c_void_p, _vp)),
     ("fdr_acoustic64_args_size", ctypes.c_size_t, ()),
     ("fdr_acoustic64_run", ctypes.c_int, (ctypes.POINTER(Acoustic64Args), _vp)),
+    ("fdr_selftest_division64", ctypes.c_int64,
+     (ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_uint32,
+      ctypes.POINTER(ctypes.c_int64))),
     ("fdr_selftest_division", ctypes.c_int64,
      (ctypes.c_int64, ctypes.c_float, ctypes.c_float, ctypes.c_uint32,
       ctypes.POINTER(ctypes.c_int64))),

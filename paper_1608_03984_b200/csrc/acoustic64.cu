@@ -268,10 +268,50 @@ A64_DEV bool arrive_is_last(uint64_t* bar) {
   return pending == 1;
 }
 
+// Correctly rounded s / m in double without __ddiv_rn's slow path for tiny
+// dividends.  In float64 the numerical precursor ahead of a wavefront decays
+// through ~1e-300 instead of underflowing to zero, and __ddiv_rn's operand
+// check sends every such dividend to its slow-path subroutine (ncu: one CALL
+// per division early in a run).  The float32 path's scaled scheme, in double:
+// s' = s 2^600 (exact, subnormals included); r = 1/m from MUFU.RCP64H and two
+// Newton steps; q = s' r plus one exact-remainder correction (correctly
+// rounded while q is normal and nothing overflows); y = q 2^-600 is kept when
+// the downscale is exact (q - y 2^600 == +0); anything else (subnormal
+// quotients, overflow, inf/NaN, m outside the normal range) takes __ddiv_rn.
+// fdr_selftest_division64 checks the bits against __ddiv_rn.
+A64_DEV double rcp_approx64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+A64_DEV double ddiv_scaled(double s, double m, bool* fast) {
+  const double sp = __dmul_rn(s, 0x1p600);
+  double r = rcp_approx64(m);
+  r = __fma_rn(r, __fma_rn(-m, r, 1.0), r);
+  r = __fma_rn(r, __fma_rn(-m, r, 1.0), r);
+  const double q0 = __dmul_rn(sp, r);
+  const double q = __fma_rn(r, __fma_rn(-m, q0, sp), q0);
+  // m > 0 on the fast path, so the quotient carries the sign of s; this only
+  // changes s = -0 (the remainder step returns +0 there, IEEE gives -0)
+  const double y = copysign(__dmul_rn(q, 0x1p-600), s);
+  const unsigned long long d = __double_as_longlong(__fma_rn(y, -0x1p600, q));
+  *fast = d == 0ull && m >= 0x1p-500 && m <= 0x1p500;
+  return y;
+}
+// Out of line on purpose: inline, the compiler if-converts the select and
+// evaluates __ddiv_rn (and its slow-path call on zero dividends) for every
+// lane (ncu: one CALL per division early in a run).
+__device__ __noinline__ double ddiv_fallback(double s, double m) { return __ddiv_rn(s, m); }
+A64_DEV double ddiv_exact(double s, double m) {
+  bool fast;
+  const double y = ddiv_scaled(s, m, &fast);
+  return fast ? y : ddiv_fallback(s, m);
+}
+
 template <bool GRID_M>
 A64_DEV double divide64(const A64Step& a, double s, double m) {
-  if (GRID_M) return __ddiv_rn(s, m);
-  if (a.m_mode == FDR_M_SCALAR) return __ddiv_rn(s, a.m_scalar);
+  if (GRID_M) return ddiv_exact(s, m);
+  if (a.m_mode == FDR_M_SCALAR) return ddiv_exact(s, a.m_scalar);
   return s;
 }
 
@@ -704,9 +744,76 @@ static int run(const fdr_acoustic64_args* a, cudaStream_t st) {
   return (2 + a->n_steps) % 3;
 }
 
+__device__ __forceinline__ uint32_t hmix(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+// ddiv_exact vs __ddiv_rn on n hashed pairs: |s| log-uniform over
+// [2^-1080, 2^520] (random mantissas, both signs, zeros, subnormals, edge
+// values), m log-uniform over [m_lo, m_hi]; counts mismatching bits and the
+// pairs that took the fast path.
+__global__ void div64_selftest_kernel(long long n, double m_lo, double m_hi, unsigned seed,
+                                      unsigned long long* bad, unsigned long long* fast) {
+  unsigned long long nb = 0, nf = 0;
+  const double lmlo = log2(m_lo), lmhi = log2(m_hi);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t h1 = hmix((uint32_t)i * 2654435761u ^ seed);
+    const uint32_t h2 = hmix(h1 ^ 0x9e3779b9u);
+    const uint32_t h3 = hmix(h2 + 0x85ebca6bu);
+    const uint32_t h4 = hmix(h3 ^ 0x27d4eb2fu);
+    double s = exp2(-1080.0 + 1600.0 * (h1 >> 8) * (1.0 / 16777216.0));
+    const unsigned long long mant = ((unsigned long long)h3 << 20) ^ h4;
+    s = __longlong_as_double((__double_as_longlong(s) & 0xfff0000000000000ull) | (mant & 0x000fffffffffffffull));
+    if ((h3 >> 24) == 0) s = 0.0;
+    if ((h3 >> 24) == 1) s = 0x1p-1074;
+    if ((h3 >> 24) == 2) s = __longlong_as_double(0x000fffffffffffffull);  // largest subnormal
+    if ((h3 >> 24) == 3) s = __longlong_as_double(0x0010000000000000ull);  // smallest normal
+    if (h2 & 1u) s = -s;
+    double m = exp2(lmlo + (lmhi - lmlo) * (h2 >> 8) * (1.0 / 16777216.0));
+    m = __longlong_as_double((__double_as_longlong(m) & 0xfff0000000000000ull) |
+                             (((unsigned long long)hmix(h4) << 21 ^ h1) & 0x000fffffffffffffull));
+    m = fmin(fmax(m, m_lo), m_hi);
+    bool f;
+    const double y = ddiv_scaled(s, m, &f);
+    nf += f;
+    const double q = f ? y : __ddiv_rn(s, m);
+    if (__double_as_longlong(q) != __double_as_longlong(__ddiv_rn(s, m))) ++nb;
+  }
+  atomicAdd(bad, nb);
+  atomicAdd(fast, nf);
+}
+
 }  // namespace fdr64
 
 extern "C" {
+
+int64_t fdr_selftest_division64(int64_t n, double m_lo, double m_hi, uint32_t seed,
+                                int64_t* n_fast) {
+  using fdr64::cuda_fail;
+  using fdr64::fail;
+  if (n <= 0 || !(m_lo > 0.0) || !(m_hi >= m_lo)) return fail(FDR_EINVAL, "bad self-test range");
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 2 * sizeof(unsigned long long));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  e = cudaMemset(d, 0, 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) {
+    fdr64::div64_selftest_kernel<<<148 * 8, 256>>>(n, m_lo, m_hi, seed, d, d + 1);
+    e = cudaGetLastError();
+  }
+  unsigned long long h[2] = {0, 0};
+  if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "float64 division self-test");
+  if (n_fast) *n_fast = (int64_t)h[1];
+  return (int64_t)h[0];
+}
+
 
 size_t fdr_acoustic64_args_size(void) { return sizeof(fdr_acoustic64_args); }
 

@@ -524,6 +524,18 @@ def selftest_division(n: int = 1 << 26, m_lo: float = 4.9e-8, m_hi: float = 4.5e
     return int(bad), int(n_fast.value)
 
 
+def selftest_division64(n: int = 1 << 26, m_lo: float = 4.9e-8, m_hi: float = 4.5e-7,
+                        seed: int = 1):
+    """The float64 kernels' scaled exact division against IEEE __ddiv_rn on
+    the GPU over n hashed operand pairs; returns (mismatches, fast_path_pairs)."""
+    lib = _lib.load()
+    n_fast = ctypes.c_int64(0)
+    bad = lib.fdr_selftest_division64(int(n), float(m_lo), float(m_hi), int(seed) & 0xffffffff,
+                                      ctypes.byref(n_fast))
+    _lib.check(int(bad) if bad < 0 else 0)
+    return int(bad), int(n_fast.value)
+
+
 def step(fld: Wavefield, cfg: KernelConfig, slabs: int = 1) -> Wavefield:
     """Advance one time step in place; returns the same Wavefield (kernel.py:176).
 

@@ -161,3 +161,18 @@ def test_gpu_f64_rejects_persistent_variant(B):
     fld = B.Wavefield.allocate(cfg.dims, cfg.halo, dtype=torch.float64)
     with pytest.raises(B.ValidationError):
         B.run(fld, cfg, variant="persistent")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m_lo,m_hi", [(4.9e-8, 4.5e-7), (0.5, 2.0), (1e-150, 1e-140),
+                                       (2.0 ** -500, 2.0 ** 500), (1e-200, 1e200)])
+def test_gpu_f64_scaled_division_matches_ieee(B, m_lo, m_hi):
+    """The a64_queue kernel's scaled exact division (fast path + __ddiv_rn
+    fallback) against IEEE __ddiv_rn bit for bit, over dividends from
+    subnormals to 2^520 and wide divisor ranges."""
+    from paper_1608_03984_b200.kernel import selftest_division64
+
+    n = 1 << 25
+    bad, n_fast = selftest_division64(n, m_lo, m_hi, seed=7)
+    assert bad == 0
+    assert n_fast > n // 8
