@@ -194,8 +194,16 @@ struct TGeo {
   static constexpr int O_IN = O_DZR + DZ;                    // cyy czz cyz (3 tiles)
   static constexpr int O_CEN = O_IN + 3 * TILE;              // k a b cxx cxy cxz prev_p prev_r
   static constexpr int STAGE = O_CEN + 8 * TILE;
+#ifdef FDR_TTI_NS
+  static constexpr int NS = FDR_TTI_NS;
+#else
   static constexpr int NS = 4;
+#endif
+#ifdef FDR_TTI_U
+  static constexpr int U = FDR_TTI_U;
+#else
   static constexpr int U = R <= 2 ? 2 * R + 1 : 3;           // planes per unrolled round
+#endif
   static constexpr int QW = 2 * R + U;                       // x-window length
   static constexpr int GW = R + U;                           // delayed in-plane window
   static constexpr int NWARPS = TNT / 32;
