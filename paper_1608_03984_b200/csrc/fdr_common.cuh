@@ -104,4 +104,38 @@ FDR_DEV void stg_stream(float* p, float4 v) {
 
 FDR_DEV float4 lds128(const float* p) { return *reinterpret_cast<const float4*>(p); }
 
+// ---- packed FP32 pairs (sm_100a FADD2 / FMUL2 / FFMA2) -------------------
+// Two floats in one 64-bit register pair, one IEEE round-to-nearest rounding
+// per lane per operation.  ptxas contracts a packed multiply feeding a packed
+// add into FFMA2 even under --fmad=false: products that a later add consumes
+// must be formed so that they cannot be fused (acoustic.cu: prod2).
+typedef unsigned long long f2;
+
+FDR_DEV f2 pk(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+FDR_DEV float lo(f2 v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+FDR_DEV float hi(f2 v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+FDR_DEV f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+FDR_DEV f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+FDR_DEV f2 mul2(f2 a, f2 b) {  // only where the product feeds no add
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+FDR_DEV f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
 }  // namespace fdr
