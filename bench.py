@@ -6,7 +6,7 @@ a 512^3 grid with the smooth random model, sponge, 15 Hz Ricker source and
 is inside the step).  `value` = whole-job grid-point updates per second
 (GPts/s) with inputs resident in HBM; `e2e` = the same metric through the
 public host-buffer API (HostSimulation.run_pipelined ->
-fdr_acoustic_run_host_async), with every simulation's H2D upload of m /
+fdr_acoustic_host_upload / _run_ws / _download), with every simulation's H2D upload of m /
 sponge / series / receivers and D2H download of the final wavefield and
 traces inside the timed region; two simulations are in flight, so one's
 copies overlap the other's time steps (back-to-back shots).  Inputs (2.1 GB of
@@ -389,8 +389,9 @@ def main():
         e2e = {"value": whole_job_rate(world, per_rank_pts, ems), "unit": UNIT,
                "h2d_bytes_per_step": sim.h2d_bytes, "d2h_bytes_per_step": sim.d2h_bytes,
                "ms_per_step": ems / args.steps, "pipeline_depth": E2E_DEPTH,
-               "api": "HostSimulation.run_pipelined -> fdr_acoustic_run_host_async (each shot "
-                      "uploads its inputs and downloads its final level and traces)"}
+               "api": "HostSimulation.run_pipelined -> fdr_acoustic_host_upload / _run_ws / "
+                      "_download (each shot uploads its inputs and downloads its final level "
+                      "and traces; steps on one stream, copies on two)"}
         del sim
 
     # per-order sweep (config 2 is a sweep over orders 2..16)
