@@ -11,6 +11,8 @@ from .kernel import (
     BenchResult,
     HostSimulation,
     KernelConfig,
+    OffGridReceivers,
+    OffGridSource,
     Receivers,
     Source,
     Sponge,
@@ -24,6 +26,7 @@ from .kernel import (
     run,
     run_benchmark,
     step,
+    trilinear_weights,
 )
 from .roofline import (MachineSpec, RooflineDataset, RooflinePoint, b200_machine, get_machine,
                        load_machines, roofline_dataset, roofline_point)

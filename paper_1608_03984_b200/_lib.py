@@ -15,7 +15,7 @@ LIB_NAME = "libb200fd.so"
 LIB_PATH = os.environ.get("B200FD_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_RADIUS = 16
 
 FDR_OK, FDR_EINVAL, FDR_ECUDA = 0, -1, -2
@@ -60,6 +60,8 @@ class AcousticArgs(ctypes.Structure):
         ("it0", _i32),
         ("n_steps", _i32),
         ("variant", _i32),
+        ("rec_w", _vp),
+        ("src_w", _vp),
     ]
 
 

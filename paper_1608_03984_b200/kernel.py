@@ -82,6 +82,48 @@ class Receivers:
         return int(self.locations.shape[0])
 
 
+def trilinear_weights(positions):
+    """Base corners (floor, int32, shape (n, 3)) and float32 weights (n, 8)
+    of off-grid positions in grid units; corner c = 4 dx + 2 dy + dz, weight
+    f32(wx * wy * wz) formed in float64."""
+    pos = np.atleast_2d(np.asarray(positions, dtype=np.float64))
+    base = np.floor(pos)
+    t = pos - base
+    w = np.empty((pos.shape[0], 8), dtype=np.float64)
+    for c in range(8):
+        dx, dy, dz = c >> 2, (c >> 1) & 1, c & 1
+        w[:, c] = ((t[:, 0] if dx else 1.0 - t[:, 0]) * (t[:, 1] if dy else 1.0 - t[:, 1])
+                   * (t[:, 2] if dz else 1.0 - t[:, 2]))
+    return base.astype(np.int32), w.astype(np.float32)
+
+
+@dataclass(frozen=True)
+class OffGridSource:
+    """Point source at a fractional grid position: each step adds
+    f32(w_c) * f32(series[it]) to the 8 surrounding points (trilinear)."""
+
+    position: tuple
+    series: np.ndarray
+
+
+@dataclass(frozen=True)
+class OffGridReceivers:
+    """Receivers at fractional grid positions (n, 3), sampled trilinearly:
+    trace = w0 u0, then trace + w_c u_c for c = 1..7, in float32."""
+
+    positions: np.ndarray
+
+    def __post_init__(self):
+        pos = np.asarray(self.positions, dtype=np.float64)
+        if pos.ndim != 2 or pos.shape[1] != 3 or pos.shape[0] < 1:
+            raise ValidationError("receiver positions must have shape (n, 3), n >= 1")
+        object.__setattr__(self, "positions", np.ascontiguousarray(pos))
+
+    @property
+    def count(self) -> int:
+        return int(self.positions.shape[0])
+
+
 @dataclass(frozen=True)
 class Sponge:
     """Separable absorbing taper G = (gx[x]*gy[y])*gz[z] applied to the new level.
@@ -133,11 +175,19 @@ class KernelConfig:
             raise ValidationError(f"interior dims {self.dims} too small for halo width {halo}")
         if not np.isscalar(self.m) and np.shape(self.m) != tuple(self.dims):
             raise ValidationError("squared-slowness grid must match interior dims")
-        if self.source is not None:
+        if isinstance(self.source, OffGridSource):
+            pos = self.source.position
+            if len(pos) != 3 or any(not 0 <= c <= d - 1 for c, d in zip(pos, self.dims)):
+                raise ValidationError(f"source position {pos} outside interior")
+        elif self.source is not None:
             loc = self.source.location
             if len(loc) != 3 or any(not 0 <= c < d for c, d in zip(loc, self.dims)):
                 raise ValidationError(f"source location {loc} outside interior")
-        if self.receivers is not None:
+        if isinstance(self.receivers, OffGridReceivers):
+            pos = self.receivers.positions
+            if (pos < 0).any() or (pos > np.asarray(self.dims) - 1).any():
+                raise ValidationError("receiver position outside interior")
+        elif self.receivers is not None:
             loc = self.receivers.locations
             if (loc < 0).any() or (loc >= np.asarray(self.dims)).any():
                 raise ValidationError("receiver location outside interior")
@@ -303,13 +353,24 @@ class _DevicePlan:
             )
         self.series = None
         self.src = (-1, 0, 0)
+        self.src_w = None
         if cfg.source is not None:
             series = np.asarray(cfg.source.series).astype(np.float32)  # kernel.py:173
             self.series = torch.from_numpy(np.ascontiguousarray(series.reshape(-1))).to(device)
-            self.src = tuple(int(c) for c in cfg.source.location)
+            if isinstance(cfg.source, OffGridSource):
+                base, w = trilinear_weights([cfg.source.position])
+                self.src = tuple(int(c) for c in base[0])
+                self.src_w = torch.from_numpy(np.ascontiguousarray(w[0])).to(device)
+            else:
+                self.src = tuple(int(c) for c in cfg.source.location)
         self.n_series = 0 if self.series is None else int(self.series.numel())
         self.rec = None
-        if cfg.receivers is not None:
+        self.rec_w = None
+        if isinstance(cfg.receivers, OffGridReceivers):
+            base, w = trilinear_weights(cfg.receivers.positions)
+            self.rec = torch.from_numpy(base.reshape(-1).copy()).to(device)
+            self.rec_w = torch.from_numpy(np.ascontiguousarray(w.reshape(-1))).to(device)
+        elif cfg.receivers is not None:
             self.rec = torch.from_numpy(cfg.receivers.locations.reshape(-1).copy()).to(device)
 
 
@@ -391,6 +452,8 @@ def run(fld: Wavefield, cfg: KernelConfig, n_steps: Optional[int] = None,
     args = _lib.AcousticArgs()
     _fill_args(args, cfg, plan, fld.dims, pitch_y, pitch_x, fld.it, n, _VARIANTS[variant])
     args.m = _ptr(plan.m_grid)
+    args.rec_w = _ptr(plan.rec_w)
+    args.src_w = _ptr(plan.src_w)
     for i in range(3):
         args.levels[i] = fld.grids[i].data_ptr()
     if plan.sponge is not None:
@@ -463,6 +526,8 @@ def _run_f64(fld: Wavefield, cfg: KernelConfig, n: int, variant: str) -> Wavefie
     dev = fld.device
     if variant == "persistent":
         raise ValidationError("the float64 path has variants auto, queue, tma and direct")
+    if isinstance(cfg.source, OffGridSource) or isinstance(cfg.receivers, OffGridReceivers):
+        raise ValidationError("the float64 path takes on-grid sources and receivers")
     pitch_y = int(fld.grids[0].shape[2])
     pitch_x = int(fld.grids[0].shape[1]) * pitch_y
     plan = getattr(cfg, "_device_plan64", None)
@@ -660,6 +725,8 @@ class HostSimulation:
     """
 
     def __init__(self, cfg: KernelConfig, variant: str = "auto", device=None):
+        if isinstance(cfg.source, OffGridSource) or isinstance(cfg.receivers, OffGridReceivers):
+            raise ValidationError("HostSimulation takes on-grid sources and receivers")
         torch = _torch()
         self.lib = _lib.load()
         self.cfg = cfg
