@@ -447,6 +447,226 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_stream(const __grid_constant__
   }
 }
 
+// ============================================================ packed kernel
+// tti_pack<R, SPONGE>: tti_stream with the two fields in the two lanes of
+// packed f32x2 registers (lane 0: p, lane 1: r).  Both fields run the same
+// derivative chains with the same weights and G coefficients, so every
+// in-plane and x derivative, window entry and G partial sum is one packed
+// value: half the arithmetic instructions at the same register count.  The
+// D1z buffer interleaves (p, r) per point.  Only L(p) and the two final
+// updates are per field (scalar, in the oracle's order).
+FDR_DEV f2 bcast(float w) { return pk(w, w); }
+FDR_DEV f2 ldpr(const float* p, const float* r, int off) { return pk(p[off], r[off]); }
+
+template <int R>
+FDR_DEV f2 d1_row2(const float* hp, const float* hr, const float* w1) {  // D1z, both fields
+  f2 d = mul2(bcast(w1[1]), sub2(ldpr(hp, hr, 1), ldpr(hp, hr, -1)));
+#pragma unroll
+  for (int j = 2; j <= R; ++j) d = fma2(bcast(w1[j]), sub2(ldpr(hp, hr, j), ldpr(hp, hr, -j)), d);
+  return d;
+}
+
+template <int R, bool SPONGE>
+__global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ TTIMaps maps,
+                                                       const TTIStep a) {
+  using G = TGeo<R>;
+  extern __shared__ __align__(128) float smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::NS * G::STAGE);
+  uint64_t* empty = full + G::NS;
+
+  gather(a);
+  const int tid = threadIdx.x;
+  const int tz = tid % TTZ, ty = tid / TTZ;
+  const int zt = blockIdx.x * TTZ, yt = blockIdx.y * TTY;
+  const int xb = blockIdx.z * a.gather_pad_chunk;
+  const int xe = min(a.nx, xb + a.gather_pad_chunk);
+  if (xb >= xe) return;
+  const int n = xe - xb;
+  const int nplanes = n + 2 * R;
+  const bool leader = (tid & 31) == 0;
+
+  auto issue = [&](int p, int s) {
+    float* st = smem + s * G::STAGE;
+    const int xn = xb - R + p;
+    const bool cen = p >= 2 * R;
+    const uint32_t bytes = 2 * G::BOX_BYTES + 3 * G::TILE * 4 + (cen ? 8 * G::TILE * 4 : 0);
+    mbar_arrive_expect_tx(&full[s], bytes);
+    tma_load_3d(st + G::O_BP, &maps.box_p, &full[s], zt - G::LZ, yt - R, xn);
+    tma_load_3d(st + G::O_BR, &maps.box_r, &full[s], zt - G::LZ, yt - R, xn);
+    tma_load_3d(st + G::O_IN + 0 * G::TILE, &maps.prm[4], &full[s], zt, yt, xn);  // cyy
+    tma_load_3d(st + G::O_IN + 1 * G::TILE, &maps.prm[5], &full[s], zt, yt, xn);  // czz
+    tma_load_3d(st + G::O_IN + 2 * G::TILE, &maps.prm[7], &full[s], zt, yt, xn);  // cyz
+    if (cen) {
+      const int xc = xn - R;
+      const int src[6] = {0, 1, 2, 3, 6, 8};  // k a b cxx cxy cxz
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+        tma_load_3d(st + G::O_CEN + i * G::TILE, &maps.prm[src[i]], &full[s], zt, yt, xc);
+      tma_load_3d(st + G::O_CEN + 6 * G::TILE, &maps.prev_p, &full[s], zt, yt, xc);
+      tma_load_3d(st + G::O_CEN + 7 * G::TILE, &maps.prev_r, &full[s], zt, yt, xc);
+    }
+  };
+  if (tid == 0) {
+    prefetch_tensormap(&maps.box_p);
+    prefetch_tensormap(&maps.box_r);
+    for (int s = 0; s < G::NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], G::NWARPS);
+    }
+    fence_barrier_init();
+    for (int p = 0; p < G::NS && p < nplanes; ++p) issue(p, p);
+  }
+  __syncthreads();
+
+  const int y = yt + ty, z = zt + tz;
+  const bool ok = y < a.ny && z < a.nz;
+  const int bown = (ty + R) * G::BZ + G::LZ + tz;
+  const int town = ty * TTZ + tz;
+  const int hrow = ty < R ? ty : (ty < 2 * R ? TTY + ty : -1);
+  float gy = 1.0f, gz = 1.0f;
+  if (SPONGE && ok) {
+    gy = a.gy[y];
+    gz = a.gz[z];
+  }
+  const bool src_here = a.sx >= 0 && y == a.sy && z == a.sz && a.it < a.n_series;
+  const float qsrc = src_here ? a.series[a.it] : 0.0f;
+  const int kinj = src_here ? a.sx - xb : -1;
+  const uint32_t px32 = (uint32_t)a.pitch_x;
+  const uint32_t oidx0 = (uint32_t)xb * px32 + (uint32_t)y * (uint32_t)a.pitch_y + (uint32_t)z;
+
+  // x windows (u, D1y u, D1z u; lane 0 p, lane 1 r): index i <-> plane p0 - 2R + i
+  f2 qu[G::QW], qy[G::QW], qz[G::QW];
+  // delayed in-plane sums: G partial (both fields), L partial (p): plane p0 - R + i
+  f2 gq[G::GW];
+  float pl[G::GW];
+#pragma unroll
+  for (int i = 0; i < G::QW; ++i) qu[i] = qy[i] = qz[i] = 0ull;
+#pragma unroll
+  for (int i = 0; i < G::GW; ++i) {
+    gq[i] = 0ull;
+    pl[i] = 0.0f;
+  }
+
+  int slot = 0;
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (int p0 = 0; p0 < nplanes; p0 += G::U) {
+#pragma unroll
+    for (int u = 0; u < G::U; ++u) {
+      const int p = p0 + u;
+      if (p >= nplanes) break;
+      mbar_wait(&full[slot], phase);
+      float* st = smem + slot * G::STAGE;
+      // ---- in-plane work on the newest plane, both fields packed
+      const float* cp = st + G::O_BP + bown;
+      const float* cr = st + G::O_BR + bown;
+      const f2 uo = ldpr(cp, cr, 0);
+      f2 dy1 = mul2(bcast(a.w1[1]), sub2(ldpr(cp, cr, G::BZ), ldpr(cp, cr, -G::BZ)));
+      f2 dyy = mul2(bcast(a.w2[0]), uo);
+#pragma unroll
+      for (int j = 1; j <= R; ++j) {
+        const f2 up = ldpr(cp, cr, j * G::BZ), um = ldpr(cp, cr, -j * G::BZ);
+        if (j >= 2) dy1 = fma2(bcast(a.w1[j]), sub2(up, um), dy1);
+        dyy = fma2(bcast(a.w2[j]), add2(up, um), dyy);
+      }
+      f2 dz1 = mul2(bcast(a.w1[1]), sub2(ldpr(cp, cr, 1), ldpr(cp, cr, -1)));
+      f2 dzz = mul2(bcast(a.w2[0]), uo);
+#pragma unroll
+      for (int j = 1; j <= R; ++j) {
+        const f2 up = ldpr(cp, cr, j), um = ldpr(cp, cr, -j);
+        if (j >= 2) dz1 = fma2(bcast(a.w1[j]), sub2(up, um), dz1);
+        dzz = fma2(bcast(a.w2[j]), add2(up, um), dzz);
+      }
+      float* dzb = st + G::O_DZP;  // interleaved (p, r) D1z rows, 2 * BY * TTZ floats
+      *reinterpret_cast<f2*>(dzb + 2 * ((ty + R) * TTZ + tz)) = dz1;
+      if (hrow >= 0)
+        *reinterpret_cast<f2*>(dzb + 2 * (hrow * TTZ + tz)) =
+            d1_row2<R>(st + G::O_BP + hrow * G::BZ + G::LZ + tz, st + G::O_BR + hrow * G::BZ + G::LZ + tz, a.w1);
+      qu[2 * R + u] = uo;
+      qy[2 * R + u] = dy1;
+      qz[2 * R + u] = dz1;
+      pl[R + u] = __fadd_rn(lo(dyy), lo(dzz));
+      // gin = fma(cyz, dyz, fma(czz, dzz, cyy dyy)): the dyz term follows the barrier
+      gq[R + u] = fma2(bcast(st[G::O_IN + 1 * G::TILE + town]), dzz, mul2(bcast(st[G::O_IN + town]), dyy));
+      __syncthreads();  // the D1z rows are complete
+      {
+        const float* db = dzb + 2 * ((ty + R) * TTZ + tz);
+        f2 dyz = mul2(bcast(a.w1[1]), sub2(*reinterpret_cast<const f2*>(db + 2 * TTZ),
+                                           *reinterpret_cast<const f2*>(db - 2 * TTZ)));
+#pragma unroll
+        for (int j = 2; j <= R; ++j)
+          dyz = fma2(bcast(a.w1[j]), sub2(*reinterpret_cast<const f2*>(db + 2 * j * TTZ),
+                                          *reinterpret_cast<const f2*>(db - 2 * j * TTZ)), dyz);
+        gq[R + u] = fma2(bcast(st[G::O_IN + 2 * G::TILE + town]), dyz, gq[R + u]);
+      }
+      // ---- the plane R behind: x derivatives and the update
+      const int k = p - 2 * R;
+      float vk = 0.f, va = 0.f, vb = 0.f, cxx = 0.f, cxy = 0.f, cxz = 0.f, ppv = 0.f, rpv = 0.f;
+      if (k >= 0) {
+        const float* cen = st + G::O_CEN + town;
+        vk = cen[0]; va = cen[G::TILE]; vb = cen[2 * G::TILE];
+        cxx = cen[3 * G::TILE]; cxy = cen[4 * G::TILE]; cxz = cen[5 * G::TILE];
+        ppv = cen[6 * G::TILE]; rpv = cen[7 * G::TILE];
+      }
+      __syncwarp();
+      if (leader && mbar_arrive_last(&empty[slot])) {
+        mbar_wait(&empty[slot], phase);
+        if (p + G::NS < nplanes) issue(p + G::NS, slot);
+      }
+      if (++slot == G::NS) {
+        slot = 0;
+        phase ^= 1u;
+      }
+      if (k >= 0) {
+        const int c = u + R;
+        f2 dxx = mul2(bcast(a.w2[0]), qu[c]);
+        f2 dxy = mul2(bcast(a.w1[1]), sub2(qy[c + 1], qy[c - 1]));
+        f2 dxz = mul2(bcast(a.w1[1]), sub2(qz[c + 1], qz[c - 1]));
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+          dxx = fma2(bcast(a.w2[j]), add2(qu[c + j], qu[c - j]), dxx);
+          if (j >= 2) {
+            dxy = fma2(bcast(a.w1[j]), sub2(qy[c + j], qy[c - j]), dxy);
+            dxz = fma2(bcast(a.w1[j]), sub2(qz[c + j], qz[c - j]), dxz);
+          }
+        }
+        const f2 gf = fma2(bcast(cxz), dxz, fma2(bcast(cxy), dxy, fma2(bcast(cxx), dxx, gq[u])));
+        const float Lp = __fadd_rn(pl[u], lo(dxx));
+        const float Hp = __fsub_rn(Lp, lo(gf));
+        const float Gr = hi(gf);
+        const float pc = lo(qu[c]), rc = hi(qu[c]);
+        float pn = __fmaf_rn(vk, __fmaf_rn(va, Hp, __fmul_rn(vb, Gr)), __fmaf_rn(2.0f, pc, -ppv));
+        float rn = __fmaf_rn(vk, __fmaf_rn(vb, Hp, Gr), __fmaf_rn(2.0f, rc, -rpv));
+        if (SPONGE) {
+          const float g = __fmul_rn(__fmul_rn(__ldg(a.gx + xb + k), gy), gz);
+          pn = __fmul_rn(pn, g);
+          rn = __fmul_rn(rn, g);
+        }
+        if (k == kinj) {
+          pn = __fadd_rn(pn, qsrc);
+          rn = __fadd_rn(rn, qsrc);
+        }
+        if (ok) {
+          const uint32_t o = oidx0 + (uint32_t)k * px32;
+          a.pn[o] = pn;
+          a.rn[o] = rn;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2 * R; ++i) {
+      qu[i] = qu[i + G::U];
+      qy[i] = qy[i + G::U];
+      qz[i] = qz[i + G::U];
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      gq[i] = gq[i + G::U];
+      pl[i] = pl[i + G::U];
+    }
+  }
+}
+
 static int tti_encode(CUtensorMap* map, const float* base, const fdr_tti_args* a, int bz, int by) {
   typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -471,12 +691,13 @@ static int tti_encode(CUtensorMap* map, const float* base, const fdr_tti_args* a
   return FDR_OK;
 }
 
-template <int R>
+template <int R, bool PACK>
 static int stream_inst(const TTIStep& s, const fdr_tti_args* a, int k, cudaStream_t st,
                        int* chunk_cache) {
   using G = TGeo<R>;
   const bool sponge = s.gx != nullptr;
-  auto kern = sponge ? tti_stream<R, true> : tti_stream<R, false>;
+  auto kern = PACK ? (sponge ? tti_pack<R, true> : tti_pack<R, false>)
+                   : (sponge ? tti_stream<R, true> : tti_stream<R, false>);
   static int configured[2] = {-1, -1};
   static int occ = 1, nsm = 148;
   int dev = 0;
@@ -522,12 +743,12 @@ static int stream_inst(const TTIStep& s, const fdr_tti_args* a, int k, cudaStrea
 }
 
 int tti_stream_launch(const TTIStep& s, const fdr_tti_args* a, int k, cudaStream_t st,
-                      int* chunk_cache) {
+                      int* chunk_cache, bool pack) {
   switch (a->order / 2) {
-    case 1: return stream_inst<1>(s, a, k, st, chunk_cache);
-    case 2: return stream_inst<2>(s, a, k, st, chunk_cache);
-    case 3: return stream_inst<3>(s, a, k, st, chunk_cache);
-    case 4: return stream_inst<4>(s, a, k, st, chunk_cache);
+    case 1: return pack ? stream_inst<1, true>(s, a, k, st, chunk_cache) : stream_inst<1, false>(s, a, k, st, chunk_cache);
+    case 2: return pack ? stream_inst<2, true>(s, a, k, st, chunk_cache) : stream_inst<2, false>(s, a, k, st, chunk_cache);
+    case 3: return pack ? stream_inst<3, true>(s, a, k, st, chunk_cache) : stream_inst<3, false>(s, a, k, st, chunk_cache);
+    case 4: return pack ? stream_inst<4, true>(s, a, k, st, chunk_cache) : stream_inst<4, false>(s, a, k, st, chunk_cache);
     default: return fail(FDR_EINVAL, "TTI stream kernel supports orders 2..8, got %d", a->order);
   }
 }
@@ -563,7 +784,7 @@ static int validate(const fdr_tti_args* a) {
     return fail(FDR_EINVAL, "source location outside interior");
   if (a->n_rec > 0 && (!a->rec_xyz || !a->traces))
     return fail(FDR_EINVAL, "receiver coordinates or trace buffer NULL");
-  if (a->variant < 0 || a->variant > FDR_VARIANT_QUEUE || a->variant == FDR_VARIANT_TMA)
+  if (a->variant < 0 || a->variant > FDR_VARIANT_QUEUE)
     return fail(FDR_EINVAL, "unknown TTI variant %d", a->variant);
   return FDR_OK;
 }
@@ -608,7 +829,7 @@ static int run(const fdr_tti_args* a, cudaStream_t st) {
   if (variant == FDR_VARIANT_AUTO)
     variant = (a->order <= 8 && (uint64_t)a->nx * (uint64_t)a->pitch_x < (1ull << 32))
                   ? FDR_VARIANT_QUEUE : FDR_VARIANT_DIRECT;
-  if (variant == FDR_VARIANT_QUEUE && a->n_steps > 0) {
+  if ((variant == FDR_VARIANT_QUEUE || variant == FDR_VARIANT_TMA) && a->n_steps > 0) {
     int rc = tti_stream_prepare(a);
     if (rc != FDR_OK) return rc;
   }
@@ -616,8 +837,9 @@ static int run(const fdr_tti_args* a, cudaStream_t st) {
   for (int k = 0; k < a->n_steps; ++k) {
     TTIStep s;
     fill(s, a, k);
-    if (variant == FDR_VARIANT_QUEUE) {
-      int rc = tti_stream_launch(s, a, k, st, &chunk);
+    if (variant == FDR_VARIANT_QUEUE || variant == FDR_VARIANT_TMA) {
+      // QUEUE: tti_pack (fields packed in f32x2 lanes); TMA: tti_stream
+      int rc = tti_stream_launch(s, a, k, st, &chunk, variant == FDR_VARIANT_QUEUE);
       if (rc != FDR_OK) return rc;
     } else {
       dim3 block(64, 4, 1), grid((a->nz + 63) / 64, (a->ny + 3) / 4, a->nx);

@@ -235,7 +235,7 @@ def _tti_key(cfg, device):
             id(cfg.sponge), str(device))
 
 
-_VARIANTS = {"auto": 0, "direct": 1, "stream": 3}
+_VARIANTS = {"auto": 0, "direct": 1, "stream": 2, "queue": 3}
 
 
 def tti_run(fld: TTIWavefield, cfg: TTIConfig, n_steps: Optional[int] = None,

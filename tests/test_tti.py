@@ -118,7 +118,7 @@ def _gpu(tti_mod, cfg, variant, n=None):
     return fld
 
 
-GPU_VARIANTS = ["stream", "direct"]
+GPU_VARIANTS = ["queue", "stream", "direct"]
 
 
 @pytest.mark.gpu

@@ -16,7 +16,7 @@ def main():
     nt = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     cfg = tti.config4(n_t=nt)
     npts = float(np.prod(cfg.dims))
-    for variant in ("stream",):
+    for variant in ("queue", "stream"):
         fld = tti.TTIWavefield.allocate(cfg.dims, cfg.halo)
         tti.tti_run(fld, cfg, 2, variant=variant)
         torch.cuda.synchronize()
