@@ -592,90 +592,66 @@ struct ElQMaps {
   CUtensorMap ctile[8]; // velocity: vx vy vz bs; stress: sxx syy szz sxy sxz syz lam mu
 };
 
-// staggered differences for the two lanes of a float2 column: p points at the
-// own pair, s = the element stride of the differenced axis (multiple of 2)
+// Staggered differences for the two lanes (2 z points of one field) in
+// packed f32x2: the oracle's per-lane sequence (mul, then fma chain; each bare
+// product feeds only an fma operand, so nothing can be contracted).
+FDR_DEV f2 f2of(float2 v) { return pk(v.x, v.y); }
+FDR_DEV float2 f2to(f2 v) { return make_float2(lo(v), hi(v)); }
+FDR_DEV f2 bcw(float c) { return pk(c, c); }
+FDR_DEV f2 ldf2(const float* p) { return *reinterpret_cast<const f2*>(p); }
+
+// p points at the own pair, s = the element stride of the differenced axis
 template <int R>
 FDR_DEV float2 pF2(const float* p, int s, const float* c) {
-  float2 a = *reinterpret_cast<const float2*>(p + s), b = *reinterpret_cast<const float2*>(p);
-  float2 d = make_float2(__fmul_rn(c[1], __fsub_rn(a.x, b.x)), __fmul_rn(c[1], __fsub_rn(a.y, b.y)));
+  f2 d = mul2(bcw(c[1]), sub2(ldf2(p + s), ldf2(p)));
 #pragma unroll
-  for (int k = 2; k <= R; ++k) {
-    a = *reinterpret_cast<const float2*>(p + k * s);
-    b = *reinterpret_cast<const float2*>(p + (1 - k) * s);
-    d = make_float2(__fmaf_rn(c[k], __fsub_rn(a.x, b.x), d.x), __fmaf_rn(c[k], __fsub_rn(a.y, b.y), d.y));
-  }
-  return d;
+  for (int k = 2; k <= R; ++k) d = fma2(bcw(c[k]), sub2(ldf2(p + k * s), ldf2(p + (1 - k) * s)), d);
+  return f2to(d);
 }
 template <int R>
 FDR_DEV float2 pB2(const float* p, int s, const float* c) {
-  float2 a = *reinterpret_cast<const float2*>(p), b = *reinterpret_cast<const float2*>(p - s);
-  float2 d = make_float2(__fmul_rn(c[1], __fsub_rn(a.x, b.x)), __fmul_rn(c[1], __fsub_rn(a.y, b.y)));
+  f2 d = mul2(bcw(c[1]), sub2(ldf2(p), ldf2(p - s)));
 #pragma unroll
-  for (int k = 2; k <= R; ++k) {
-    a = *reinterpret_cast<const float2*>(p + (k - 1) * s);
-    b = *reinterpret_cast<const float2*>(p - k * s);
-    d = make_float2(__fmaf_rn(c[k], __fsub_rn(a.x, b.x), d.x), __fmaf_rn(c[k], __fsub_rn(a.y, b.y), d.y));
-  }
-  return d;
+  for (int k = 2; k <= R; ++k) d = fma2(bcw(c[k]), sub2(ldf2(p + (k - 1) * s), ldf2(p - k * s)), d);
+  return f2to(d);
 }
-// along z within one row window w[] (w[LZ] = the own pair's first point)
+// along z within one row window w[] (w[LZ] = the own pair's first point); the
+// odd-offset pairs are misaligned, so the lane differences are scalar
 template <int R, int LZ>
 FDR_DEV float2 zF2(const float* w, const float* c) {
-  float2 d;
+  f2 d = mul2(bcw(c[1]), pk(__fsub_rn(w[LZ + 1], w[LZ]), __fsub_rn(w[LZ + 2], w[LZ + 1])));
 #pragma unroll
-  for (int l = 0; l < 2; ++l) {
-    const int i = LZ + l;
-    float v = __fmul_rn(c[1], __fsub_rn(w[i + 1], w[i]));
-#pragma unroll
-    for (int k = 2; k <= R; ++k) v = __fmaf_rn(c[k], __fsub_rn(w[i + k], w[i + 1 - k]), v);
-    (l == 0 ? d.x : d.y) = v;
-  }
-  return d;
+  for (int k = 2; k <= R; ++k)
+    d = fma2(bcw(c[k]), pk(__fsub_rn(w[LZ + k], w[LZ + 1 - k]), __fsub_rn(w[LZ + 1 + k], w[LZ + 2 - k])), d);
+  return f2to(d);
 }
 template <int R, int LZ>
 FDR_DEV float2 zB2(const float* w, const float* c) {
-  float2 d;
+  f2 d = mul2(bcw(c[1]), pk(__fsub_rn(w[LZ], w[LZ - 1]), __fsub_rn(w[LZ + 1], w[LZ])));
 #pragma unroll
-  for (int l = 0; l < 2; ++l) {
-    const int i = LZ + l;
-    float v = __fmul_rn(c[1], __fsub_rn(w[i], w[i - 1]));
-#pragma unroll
-    for (int k = 2; k <= R; ++k) v = __fmaf_rn(c[k], __fsub_rn(w[i + k - 1], w[i - k]), v);
-    (l == 0 ? d.x : d.y) = v;
-  }
-  return d;
+  for (int k = 2; k <= R; ++k)
+    d = fma2(bcw(c[k]), pk(__fsub_rn(w[LZ + k - 1], w[LZ - k]), __fsub_rn(w[LZ + k], w[LZ + 1 - k])), d);
+  return f2to(d);
 }
 // along x from a register queue of float2 (centre index cidx)
 template <int R, int QD, bool ROT>
 FDR_DEV float2 xF2(const float2* q, int cidx, const float* c) {
-  auto at = [&](int i) -> float2 { return q[ROT ? (i + QD) % QD : i]; };
-  float2 a = at(cidx + 1), b = at(cidx);
-  float2 d = make_float2(__fmul_rn(c[1], __fsub_rn(a.x, b.x)), __fmul_rn(c[1], __fsub_rn(a.y, b.y)));
+  auto at = [&](int i) -> f2 { return f2of(q[ROT ? (i + QD) % QD : i]); };
+  f2 d = mul2(bcw(c[1]), sub2(at(cidx + 1), at(cidx)));
 #pragma unroll
-  for (int k = 2; k <= R; ++k) {
-    a = at(cidx + k);
-    b = at(cidx + 1 - k);
-    d = make_float2(__fmaf_rn(c[k], __fsub_rn(a.x, b.x), d.x), __fmaf_rn(c[k], __fsub_rn(a.y, b.y), d.y));
-  }
-  return d;
+  for (int k = 2; k <= R; ++k) d = fma2(bcw(c[k]), sub2(at(cidx + k), at(cidx + 1 - k)), d);
+  return f2to(d);
 }
 template <int R, int QD, bool ROT>
 FDR_DEV float2 xB2(const float2* q, int cidx, const float* c) {
-  auto at = [&](int i) -> float2 { return q[ROT ? (i + QD) % QD : i]; };
-  float2 a = at(cidx), b = at(cidx - 1);
-  float2 d = make_float2(__fmul_rn(c[1], __fsub_rn(a.x, b.x)), __fmul_rn(c[1], __fsub_rn(a.y, b.y)));
+  auto at = [&](int i) -> f2 { return f2of(q[ROT ? (i + QD) % QD : i]); };
+  f2 d = mul2(bcw(c[1]), sub2(at(cidx), at(cidx - 1)));
 #pragma unroll
-  for (int k = 2; k <= R; ++k) {
-    a = at(cidx + k - 1);
-    b = at(cidx - k);
-    d = make_float2(__fmaf_rn(c[k], __fsub_rn(a.x, b.x), d.x), __fmaf_rn(c[k], __fsub_rn(a.y, b.y), d.y));
-  }
-  return d;
+  for (int k = 2; k <= R; ++k) d = fma2(bcw(c[k]), sub2(at(cidx + k - 1), at(cidx - k)), d);
+  return f2to(d);
 }
-FDR_DEV float2 add2f(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
-FDR_DEV float2 fma2f(float2 a, float2 b, float2 c) {
-  return make_float2(__fmaf_rn(a.x, b.x, c.x), __fmaf_rn(a.y, b.y, c.y));
-}
+FDR_DEV float2 add2f(float2 a, float2 b) { return f2to(add2(f2of(a), f2of(b))); }
+FDR_DEV float2 fma2f(float2 a, float2 b, float2 c) { return f2to(fma2(f2of(a), f2of(b), f2of(c))); }
 FDR_DEV void stg2cs(float* p, float2 v) {
   asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
@@ -847,7 +823,7 @@ __global__ void __launch_bounds__(QN, 2) el_queue(const __grid_constant__ ElQMap
           const float gxy = __fmul_rn(__ldg(a.gx + xb + k), gy);
           const float g0 = __fmul_rn(gxy, gz0), g1 = __fmul_rn(gxy, gz1);
 #pragma unroll
-          for (int i = 0; i < NO; ++i) out[i] = make_float2(__fmul_rn(out[i].x, g0), __fmul_rn(out[i].y, g1));
+          for (int i = 0; i < NO; ++i) out[i] = f2to(mul2(f2of(out[i]), pk(g0, g1)));
         }
         if (PASS == 1 && k == kinj) {
 #pragma unroll
