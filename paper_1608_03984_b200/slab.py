@@ -16,6 +16,16 @@ on the global faces, where the kernels' zero fill is the reference halo):
 * the source is injected by its owner only, receivers are recorded by their
   owners (traces gathered back into global order).
 
+Off-grid (trilinear) positions: the source goes to every slab whose owned
+planes hold one of its corners (a corner on a ghost plane is overwritten by
+the exchange).  A receiver belongs to the slab owning its base plane floor(x);
+its upper corner plane may be the first ghost plane, which is sampled inside
+the step, before the exchange.  With ghost width r + 1 that plane's update is
+exact (its stencil stays within the ghosts, its previous level was exchanged
+the step before), so off-grid receivers need `slab_halo(cfg)` = r + 1 ghost
+planes.  Local positions are pos - gx0, exact in float64, so the trilinear
+weights are unchanged.
+
 The result is bit-identical to the single-grid run: the same arithmetic on the
 same values at every owned point.  `SlabPlan` and the exchange are plain host
 logic (tests/test_slab.py runs them with the numpy oracle on gloo ranks);
@@ -28,7 +38,7 @@ from typing import Optional
 import numpy as np
 
 from .errors import ValidationError
-from .kernel import KernelConfig, Receivers, Source, Sponge
+from .kernel import KernelConfig, OffGridReceivers, OffGridSource, Receivers, Source, Sponge
 
 
 @dataclass(frozen=True)
@@ -83,9 +93,18 @@ class SlabPlan:
         return out
 
 
+def slab_halo(cfg: KernelConfig) -> int:
+    """Ghost planes per internal face that make the decomposition exact: the
+    stencil radius, plus one for off-grid receivers (module docstring)."""
+    return cfg.halo + (1 if isinstance(cfg.receivers, OffGridReceivers) else 0)
+
+
 def slab_config(cfg: KernelConfig, plan: SlabPlan, i: int):
     """Slab i's KernelConfig (local dims, m / sponge slices, owner-only source
     and receivers) and the global indices of its receivers."""
+    if plan.n_slabs > 1 and plan.halo < slab_halo(cfg):
+        raise ValidationError(f"plan has {plan.halo} ghost planes; this config needs "
+                              f"slab_halo(cfg) = {slab_halo(cfg)}")
     gx0, gx1 = plan.local_range(i)
     x0, x1 = plan.span(i)
     ny, nz = cfg.dims[1], cfg.dims[2]
@@ -94,18 +113,25 @@ def slab_config(cfg: KernelConfig, plan: SlabPlan, i: int):
     if cfg.sponge is not None:
         sponge = Sponge(cfg.sponge.x[gx0:gx1], cfg.sponge.y, cfg.sponge.z)
     source = None
-    if cfg.source is not None and x0 <= cfg.source.location[0] < x1:
+    if isinstance(cfg.source, OffGridSource):
+        px, py, pz = (float(c) for c in cfg.source.position)
+        bx = int(np.floor(px))
+        if bx + 1 >= x0 and bx < x1:  # a corner plane is owned here
+            source = OffGridSource((px - gx0, py, pz), cfg.source.series)
+    elif cfg.source is not None and x0 <= cfg.source.location[0] < x1:
         sx, sy, sz = cfg.source.location
         source = Source((sx - gx0, sy, sz), cfg.source.series)
     receivers, rec_index = None, np.zeros(0, dtype=np.int64)
     if cfg.receivers is not None:
-        loc = cfg.receivers.locations
-        mine = (loc[:, 0] >= x0) & (loc[:, 0] < x1)
+        off = isinstance(cfg.receivers, OffGridReceivers)
+        loc = cfg.receivers.positions if off else cfg.receivers.locations
+        base = np.floor(loc[:, 0]) if off else loc[:, 0]
+        mine = (base >= x0) & (base < x1)
         rec_index = np.nonzero(mine)[0]
         if rec_index.size:
             local = loc[mine].copy()
             local[:, 0] -= gx0
-            receivers = Receivers(local)
+            receivers = OffGridReceivers(local) if off else Receivers(local)
     local = KernelConfig(order=cfg.order, dims=(gx1 - gx0, ny, nz), n_t=cfg.n_t, dt=cfg.dt, h=cfg.h,
                          m=m, source=source, receivers=receivers, sponge=sponge)
     return local, rec_index

@@ -17,14 +17,14 @@ def main():
     import torch.distributed as dist
 
     from oracle import acoustic as O
-    from paper_1608_03984_b200.slab import SlabPlan, exchange, slab_config
+    from paper_1608_03984_b200.slab import SlabPlan, exchange, slab_config, slab_halo
     from slab_cases import slab_case
 
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     results = {}
     for name, (cfg, nsteps) in slab_case().items():
-        plan = SlabPlan(cfg.dims[0], world, cfg.halo)
+        plan = SlabPlan(cfg.dims[0], world, slab_halo(cfg))
         local, rec_index = slab_config(cfg, plan, rank)
         st = O.OracleState(local.dims, local.halo)
         if local.receivers is not None:

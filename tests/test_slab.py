@@ -12,7 +12,7 @@ import pytest
 
 from oracle import acoustic as O
 from paper_1608_03984_b200.errors import ValidationError
-from paper_1608_03984_b200.slab import SlabPlan, exchange_local, slab_config
+from paper_1608_03984_b200.slab import SlabPlan, exchange_local, slab_config, slab_halo
 from slab_cases import slab_case
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -48,25 +48,68 @@ def test_slab_config_owner_only_source_and_receivers():
     assert np.array_equal(b.m, cfg.m[10:24])
 
 
-@pytest.mark.parametrize("n_slabs", [2, 3])
-def test_local_exchange_oracle_bitexact(n_slabs):
-    """All slabs in one process (numpy oracle + exchange_local) == full grid."""
+def oracle_slabs(cfg, plan, n):
+    """All slabs in one process (numpy oracle + exchange_local): the global
+    final level and traces."""
     import torch
 
+    parts = [slab_config(cfg, plan, i) for i in range(plan.n_slabs)]
+    states = [O.OracleState(c.dims, c.halo) for c, _ in parts]
+    for (c, _), st in zip(parts, states):
+        if c.receivers is not None:
+            st.traces = np.zeros((cfg.n_t, c.receivers.count), np.float32)
+    tapers = [O.sponge_taper(c) for c, _ in parts]
+    r = cfg.halo
+    for _ in range(n):
+        for (c, _), st, tp in zip(parts, states, tapers):
+            O.step(st, c, taper=tp)
+        exchange_local([torch.from_numpy(st.grids[2])[r: r + c.dims[0]]
+                        for (c, _), st in zip(parts, states)], plan)
+    got = np.concatenate([O.interior(st.grids[2], r)[plan.owned_local(i)]
+                          for i, st in enumerate(states)])
+    traces = np.zeros((cfg.n_t, cfg.receivers.count), np.float32)
+    for (c, idx), st in zip(parts, states):
+        if idx.size:
+            traces[:, idx] = st.traces
+    return got, traces
+
+
+@pytest.mark.parametrize("n_slabs", [2, 3])
+def test_local_exchange_oracle_bitexact(n_slabs):
+    """All slabs in one process == full grid, field and traces (on- and off-grid)."""
     for cfg, n in slab_case().values():
-        plan = SlabPlan(cfg.dims[0], n_slabs, cfg.halo)
-        parts = [slab_config(cfg, plan, i) for i in range(n_slabs)]
-        states = [O.OracleState(c.dims, c.halo) for c, _ in parts]
-        tapers = [O.sponge_taper(c) for c, _ in parts]
-        r = cfg.halo
-        for _ in range(n):
-            for (c, _), st, tp in zip(parts, states, tapers):
-                O.step(st, c, taper=tp)
-            exchange_local([torch.from_numpy(st.grids[2])[r: r + c.dims[0]]
-                            for (c, _), st in zip(parts, states)], plan)
-        got = np.concatenate([O.interior(st.grids[2], r)[plan.owned_local(i)]
-                              for i, st in enumerate(states)])
-        assert np.array_equal(got, O.simulate(cfg, n).latest())
+        got, traces = oracle_slabs(cfg, SlabPlan(cfg.dims[0], n_slabs, slab_halo(cfg)), n)
+        full = O.simulate(cfg, n)
+        assert np.array_equal(got, full.latest())
+        assert np.array_equal(traces, full.traces) and np.abs(full.traces).max() > 0
+
+
+def test_offgrid_needs_the_wider_ghost_layer():
+    cfg, n = slab_case()["off8"]
+    assert slab_halo(cfg) == cfg.halo + 1 and slab_halo(slab_case()["o8"][0]) == 4
+    with pytest.raises(ValidationError, match="slab_halo"):
+        slab_config(cfg, SlabPlan(cfg.dims[0], 2, cfg.halo), 0)
+    # the straddling source goes to both slabs, each receiver to exactly one
+    plan = SlabPlan(cfg.dims[0], 2, slab_halo(cfg))
+    (a, ia), (b, ib) = slab_config(cfg, plan, 0), slab_config(cfg, plan, 1)
+    assert a.source.position[0] == 14.37 and b.source.position[0] == 14.37 - 10
+    assert sorted(np.concatenate([ia, ib]).tolist()) == list(range(cfg.receivers.count))
+    assert np.floor(b.receivers.positions[:, 0]).min() >= 5  # base plane owned by slab 1
+
+
+def test_offgrid_receivers_wrong_with_only_r_ghost_planes(monkeypatch):
+    """Why r + 1: with r ghost planes the receivers whose upper corner plane is
+    the first ghost plane (x 14.6 for 2 slabs) sample a not-yet-exchanged,
+    truncated-stencil value and diverge; everything else stays exact."""
+    import paper_1608_03984_b200.slab as S
+
+    cfg, n = slab_case()["off4"]
+    monkeypatch.setattr(S, "slab_halo", lambda c: c.halo)
+    got, traces = oracle_slabs(cfg, SlabPlan(cfg.dims[0], 2, cfg.halo), n)
+    full = O.simulate(cfg, n)
+    assert np.array_equal(got, full.latest())
+    bad = np.nonzero((traces != full.traces).any(0))[0]
+    assert cfg.receivers.positions[bad, 0].tolist() == [14.6]
 
 
 def _free_port():
@@ -84,7 +127,7 @@ def test_two_rank_gloo_halo_exchange(tmp_path):
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-3000:]
     res = json.loads(out.read_text())
-    assert set(res) == {"o4", "o8"}
+    assert set(res) == set(slab_case())
     for name, v in res.items():
         assert v == {"field_equal": True, "traces_equal": True, "nonzero": True}, name
 
@@ -98,7 +141,7 @@ def test_gpu_slabs_local_bitexact(cuda_device, n_slabs):
     from paper_1608_03984_b200.slab import run_slabs_local
 
     for cfg, n in slab_case().values():
-        plan = SlabPlan(cfg.dims[0], n_slabs, cfg.halo)
+        plan = SlabPlan(cfg.dims[0], n_slabs, slab_halo(cfg))
         got, traces = run_slabs_local(cfg, plan, n)
         fld = B.Wavefield.allocate(cfg.dims, cfg.halo)
         B.run(fld, cfg, n)
