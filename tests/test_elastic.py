@@ -89,8 +89,8 @@ GPU_VARIANTS = ["queue", "stream", "direct"]
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("variant", GPU_VARIANTS)
-@pytest.mark.parametrize("order,dims", [(2, (11, 12, 13)), (4, (17, 16, 15)), (8, (24, 22, 20)),
-                                        (8, (33, 30, 37))])
+@pytest.mark.parametrize("order,dims", [(2, (11, 12, 13)), (4, (17, 16, 15)), (6, (19, 18, 21)),
+                                        (8, (24, 22, 20)), (8, (33, 30, 37))])
 def test_gpu_elastic_bitexact_vs_c_oracle(el_mod, variant, order, dims):
     cfg = small_cfg(order=order, dims=dims, n_t=12)
     fld = el_mod.ElasticWavefield.allocate(cfg.dims, cfg.halo)
@@ -99,6 +99,25 @@ def test_gpu_elastic_bitexact_vs_c_oracle(el_mod, variant, order, dims):
     for k in FIELDS:
         assert sha(fld.numpy(k)) == sha(st.interior(k)), k
     assert (fld.traces.cpu().numpy() == st.traces).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [12, 16])
+def test_gpu_elastic_high_orders_bitexact(el_mod, order):
+    """Orders above 8 run the direct kernel (AUTO); the streaming variants
+    reject them with the reference's ValidationError."""
+    from paper_1608_03984_b200.errors import ValidationError
+
+    cfg = small_cfg(order=order, dims=(order + 3, order + 2, order + 5), n_t=8)
+    fld = el_mod.ElasticWavefield.allocate(cfg.dims, cfg.halo)
+    el_mod.elastic_run(fld, cfg, variant="auto")
+    st = E.simulate_c(cfg, cfg.params(), elastic_weights_f32(order))
+    for k in FIELDS:
+        assert sha(fld.numpy(k)) == sha(st.interior(k)), k
+    assert (fld.traces.cpu().numpy() == st.traces).all()
+    assert np.abs(st.interior("vz")).max() > 0
+    with pytest.raises(ValidationError):
+        el_mod.elastic_run(el_mod.ElasticWavefield.allocate(cfg.dims, cfg.halo), cfg, variant="queue")
 
 
 @pytest.mark.gpu

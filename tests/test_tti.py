@@ -123,8 +123,8 @@ GPU_VARIANTS = ["queue", "stream", "direct"]
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("variant", GPU_VARIANTS)
-@pytest.mark.parametrize("order,dims", [(2, (11, 12, 13)), (4, (17, 16, 15)), (8, (24, 22, 20)),
-                                        (8, (33, 30, 37))])
+@pytest.mark.parametrize("order,dims", [(2, (11, 12, 13)), (4, (17, 16, 15)), (6, (19, 18, 21)),
+                                        (8, (24, 22, 20)), (8, (33, 30, 37))])
 def test_gpu_tti_bitexact_vs_c_oracle(tti_mod, variant, order, dims):
     cfg = small_cfg(order=order, dims=dims, n_t=12)
     fld = _gpu(tti_mod, cfg, variant)
@@ -134,6 +134,25 @@ def test_gpu_tti_bitexact_vs_c_oracle(tti_mod, variant, order, dims):
     assert sha(fld.numpy("r")) == sha(st.interior("r"))
     assert sha(fld.numpy("p", 1)) == sha(st.interior("p", 1))
     assert (fld.traces.cpu().numpy() == st.traces).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [12, 16])
+def test_gpu_tti_high_orders_bitexact(tti_mod, order):
+    """Orders above 8 run the direct kernel (AUTO); the streaming variants
+    reject them with the reference's ValidationError."""
+    from paper_1608_03984_b200.errors import ValidationError
+
+    cfg = small_cfg(order=order, dims=(order + 3, order + 2, order + 5), n_t=8)
+    fld = _gpu(tti_mod, cfg, "auto")
+    w2, w1 = tti_weights_f32(order)
+    st = T.simulate_c(cfg, cfg.params(), w2, w1)
+    assert sha(fld.numpy("p")) == sha(st.interior("p"))
+    assert sha(fld.numpy("r")) == sha(st.interior("r"))
+    assert (fld.traces.cpu().numpy() == st.traces).all()
+    assert np.abs(st.interior("p")).max() > 0
+    with pytest.raises(ValidationError):
+        _gpu(tti_mod, cfg, "queue")
 
 
 @pytest.mark.gpu
