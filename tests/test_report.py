@@ -79,7 +79,9 @@ def test_svg_chart_well_formed(tmp_path):
     assert len(root.findall(ns + "polyline")) == 1
     assert len(root.findall(ns + "circle")) == 2 and len(root.findall(ns + "rect")) == 3
     text = " ".join(t.text or "" for t in root.iter(ns + "text"))
-    assert "6,557.4 GB/s" in text and "acoustic:k9 82%" in text
+    bw = m.peak_bw_achievable  # the measured HBM rate (MEASURED_PEAKS.json) when present
+    pct = round(100 * p.measured_gflops / p.attainable_gflops)
+    assert f"{bw:,.1f} GB/s" in text and f"acoustic:k9 {pct}%" in text
     out = tmp_path / "r.svg"
     charts.write_svg(svg, out)
     assert out.read_text() == svg
