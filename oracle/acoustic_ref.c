@@ -85,6 +85,7 @@ int fdo_acoustic_run(int order, int nx, int ny, int nz, const float* w, float co
   if (threads > nx) threads = nx;
   pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
   slab_job* jobs = (slab_job*)malloc(sizeof(slab_job) * threads);
+  char* started = (char*)malloc(threads);
   for (int k = 0; k < n_steps; ++k) {
     float* out = lv[(0 + k) % 3];
     const float* prev = lv[(1 + k) % 3];
@@ -110,13 +111,12 @@ int fdo_acoustic_run(int order, int nx, int ny, int nz, const float* w, float co
       j->gz = gz;
       j->x_lo = (int)((long)t * nx / threads);
       j->x_hi = (int)((long)(t + 1) * nx / threads);
-      if (threads > 1)
-        pthread_create(&tid[t], 0, run_slab, j);
-      else
-        run_slab(j);
+      /* a slab whose thread cannot be created runs inline (never skipped) */
+      started[t] = threads > 1 && pthread_create(&tid[t], 0, run_slab, j) == 0;
+      if (!started[t]) run_slab(j);
     }
-    if (threads > 1)
-      for (int t = 0; t < threads; ++t) pthread_join(tid[t], 0);
+    for (int t = 0; t < threads; ++t)
+      if (started[t]) pthread_join(tid[t], 0);
     const int it = it0 + k;
     if (sx_ >= 0 && series && it < n_series) {
       float* p = out + (long)(sx_ + r) * sx + (long)(sy_ + r) * sy + (sz_ + r);
@@ -131,5 +131,6 @@ int fdo_acoustic_run(int order, int nx, int ny, int nz, const float* w, float co
   }
   free(tid);
   free(jobs);
+  free(started);
   return (2 + n_steps) % 3;
 }

@@ -124,15 +124,16 @@ static void* run_slab(void* arg) {
 }
 
 static void run_pass(el_job* jobs, pthread_t* tid, int threads, int pass) {
+  char* started = (char*)malloc(threads);
   for (int t = 0; t < threads; ++t) {
     jobs[t].pass = pass;
-    if (threads > 1)
-      pthread_create(&tid[t], 0, run_slab, &jobs[t]);
-    else
-      run_slab(&jobs[t]);
+    /* a slab whose thread cannot be created runs inline (never skipped) */
+    started[t] = threads > 1 && pthread_create(&tid[t], 0, run_slab, &jobs[t]) == 0;
+    if (!started[t]) run_slab(&jobs[t]);
   }
-  if (threads > 1)
-    for (int t = 0; t < threads; ++t) pthread_join(tid[t], 0);
+  for (int t = 0; t < threads; ++t)
+    if (started[t]) pthread_join(tid[t], 0);
+  free(started);
 }
 
 /* The velocity pass reads stresses only (plus its own v), the stress pass

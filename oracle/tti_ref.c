@@ -130,6 +130,7 @@ int fdo_tti_run(int order, int nx, int ny, int nz, const float* w2, const float*
   if (threads > nx) threads = nx;
   pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
   tti_job* jobs = (tti_job*)malloc(sizeof(tti_job) * threads);
+  char* started = (char*)malloc(threads);
   for (int k = 0; k < n_steps; ++k) {
     const int io = (0 + k) % 3, ip = (1 + k) % 3, ic = (2 + k) % 3;
     for (int t = 0; t < threads; ++t) {
@@ -154,13 +155,12 @@ int fdo_tti_run(int order, int nx, int ny, int nz, const float* w2, const float*
       j->gz = gz;
       j->x_lo = (int)((long)t * nx / threads);
       j->x_hi = (int)((long)(t + 1) * nx / threads);
-      if (threads > 1)
-        pthread_create(&tid[t], 0, run_slab, j);
-      else
-        run_slab(j);
+      /* a slab whose thread cannot be created runs inline (never skipped) */
+      started[t] = threads > 1 && pthread_create(&tid[t], 0, run_slab, j) == 0;
+      if (!started[t]) run_slab(j);
     }
-    if (threads > 1)
-      for (int t = 0; t < threads; ++t) pthread_join(tid[t], 0);
+    for (int t = 0; t < threads; ++t)
+      if (started[t]) pthread_join(tid[t], 0);
     const int it = it0 + k;
     const long o = (long)(sx_ + r) * sx + (long)(sy_ + r) * sy + (sz_ + r);
     if (sx_ >= 0 && series && it < n_series) {
@@ -175,5 +175,6 @@ int fdo_tti_run(int order, int nx, int ny, int nz, const float* w2, const float*
   }
   free(tid);
   free(jobs);
+  free(started);
   return (2 + n_steps) % 3;
 }
