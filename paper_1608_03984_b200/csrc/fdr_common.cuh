@@ -104,6 +104,27 @@ FDR_DEV void stg_stream(float* p, float4 v) {
 
 FDR_DEV float4 lds128(const float* p) { return *reinterpret_cast<const float4*>(p); }
 
+// Register copy pinned to the ALU pipe.  ptxas emits plain copies as
+// IMAD.MOV (FMA pipe, 2 cycles per warp instruction) about half the time;
+// in the streaming kernels the FMA pipe carries all the arithmetic, so the
+// register-queue shifts go through an identity PRMT instead (ALU pipe).
+FDR_DEV float alu_mov(float x) {
+  uint32_t r;
+  asm volatile("prmt.b32 %0, %1, 0, 0x3210;" : "=r"(r) : "r"(__float_as_uint(x)));
+  return __uint_as_float(r);
+}
+FDR_DEV float4 alu_mov4(float4 v) {
+  return make_float4(alu_mov(v.x), alu_mov(v.y), alu_mov(v.z), alu_mov(v.w));
+}
+// Queue-shift copy of the float32 acoustic kernel; -DFDR_PLAIN_QMOV builds
+// plain copies for A/B.  Measured: +1-3% at acoustic orders
+// 8-16; the same change cost TTI 10% and float64 2%, so those keep plain copies.
+#ifdef FDR_PLAIN_QMOV
+FDR_DEV float4 qmov(float4 v) { return v; }
+#else
+FDR_DEV float4 qmov(float4 v) { return alu_mov4(v); }
+#endif
+
 // ---- packed FP32 pairs (sm_100a FADD2 / FMUL2 / FFMA2) -------------------
 // Two floats in one 64-bit register pair, one IEEE round-to-nearest rounding
 // per lane per operation.  ptxas contracts a packed multiply feeding a packed
