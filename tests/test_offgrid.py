@@ -87,6 +87,8 @@ def test_gpu_offgrid_small_grid_and_stepwise(cuda_device):
     assert (a.traces.cpu().numpy() == st.traces).all()
     with pytest.raises(B.ValidationError):
         B.run(B.Wavefield.allocate(cfg.dims, cfg.halo), cfg, variant="persistent")
+    with pytest.raises(B.ValidationError, match="on-grid"):
+        B.run(B.Wavefield.allocate(cfg.dims, cfg.halo), cfg, variant="cluster")
 
 
 @pytest.mark.gpu
