@@ -74,6 +74,23 @@ class ClockSampler:
         self._t = None
 
     def _loop(self):
+        try:  # in-process NVML: microseconds per sample, no process spawn beside the timed work
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(sm), str(mx)] + ["Active" if rs & b else "Not Active" for b in bits])
+                self._stop.wait(0.02)
+            pynvml.nvmlShutdown()
+            return
+        except Exception:  # noqa: BLE001  (no NVML binding: fall back to nvidia-smi)
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
