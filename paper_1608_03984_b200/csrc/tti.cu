@@ -207,7 +207,7 @@ struct TGeo {
   static constexpr int QW = 2 * R + U;                       // x-window length
   static constexpr int GW = R + U;                           // delayed in-plane window
   static constexpr int NWARPS = TNT / 32;
-  static constexpr size_t SMEM = size_t(NS) * STAGE * 4 + 2 * NS * 8;
+  static constexpr size_t SMEM = size_t(NS) * STAGE * 4 + 3 * NS * 8;  // full, empty, D1z-ready
 };
 
 struct TTIMaps {
@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
   extern __shared__ __align__(128) float smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::NS * G::STAGE);
   uint64_t* empty = full + G::NS;
+  uint64_t* dzrdy = empty + G::NS;  // per stage: every warp's D1z rows are written
 
   gather(a);
   const int tid = threadIdx.x;
@@ -512,6 +513,7 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
     for (int s = 0; s < G::NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], G::NWARPS);
+      mbar_init(&dzrdy[s], G::NWARPS);
     }
     fence_barrier_init();
     for (int p = 0; p < G::NS && p < nplanes; ++p) issue(p, p);
@@ -588,36 +590,19 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
       pl[R + u] = __fadd_rn(lo(dyy), lo(dzz));
       // gin = fma(cyz, dyz, fma(czz, dzz, cyy dyy)): the dyz term follows the barrier
       gq[R + u] = fma2(bcast(st[G::O_IN + 1 * G::TILE + town]), dzz, mul2(bcast(st[G::O_IN + town]), dyy));
-      __syncthreads();  // the D1z rows are complete
-      {
-        const float* db = dzb + 2 * ((ty + R) * TTZ + tz);
-        f2 dyz = mul2(bcast(a.w1[1]), sub2(*reinterpret_cast<const f2*>(db + 2 * TTZ),
-                                           *reinterpret_cast<const f2*>(db - 2 * TTZ)));
-#pragma unroll
-        for (int j = 2; j <= R; ++j)
-          dyz = fma2(bcast(a.w1[j]), sub2(*reinterpret_cast<const f2*>(db + 2 * j * TTZ),
-                                          *reinterpret_cast<const f2*>(db - 2 * j * TTZ)), dyz);
-        gq[R + u] = fma2(bcast(st[G::O_IN + 2 * G::TILE + town]), dyz, gq[R + u]);
-      }
+      // Split barrier: announce this warp's D1z rows, update the plane R
+      // behind (which needs no D1z row of this plane), then wait for every
+      // warp's rows.  The warps' skew is absorbed by useful work instead of a
+      // __syncthreads.
+      __syncwarp();
+      if (leader) mbar_arrive_t(&dzrdy[slot]);
       // ---- the plane R behind: x derivatives and the update
       const int k = p - 2 * R;
-      float vk = 0.f, va = 0.f, vb = 0.f, cxx = 0.f, cxy = 0.f, cxz = 0.f, ppv = 0.f, rpv = 0.f;
       if (k >= 0) {
         const float* cen = st + G::O_CEN + town;
-        vk = cen[0]; va = cen[G::TILE]; vb = cen[2 * G::TILE];
-        cxx = cen[3 * G::TILE]; cxy = cen[4 * G::TILE]; cxz = cen[5 * G::TILE];
-        ppv = cen[6 * G::TILE]; rpv = cen[7 * G::TILE];
-      }
-      __syncwarp();
-      if (leader && mbar_arrive_last(&empty[slot])) {
-        mbar_wait(&empty[slot], phase);
-        if (p + G::NS < nplanes) issue(p + G::NS, slot);
-      }
-      if (++slot == G::NS) {
-        slot = 0;
-        phase ^= 1u;
-      }
-      if (k >= 0) {
+        const float vk = cen[0], va = cen[G::TILE], vb = cen[2 * G::TILE];
+        const float cxx = cen[3 * G::TILE], cxy = cen[4 * G::TILE], cxz = cen[5 * G::TILE];
+        const float ppv = cen[6 * G::TILE], rpv = cen[7 * G::TILE];
         const int c = u + R;
         f2 dxx = mul2(bcast(a.w2[0]), qu[c]);
         f2 dxy = mul2(bcast(a.w1[1]), sub2(qy[c + 1], qy[c - 1]));
@@ -651,6 +636,27 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
           a.pn[o] = pn;
           a.rn[o] = rn;
         }
+      }
+      mbar_wait(&dzrdy[slot], phase);  // the D1z rows are complete
+      {
+        const float* db = dzb + 2 * ((ty + R) * TTZ + tz);
+        f2 dyz = mul2(bcast(a.w1[1]), sub2(*reinterpret_cast<const f2*>(db + 2 * TTZ),
+                                           *reinterpret_cast<const f2*>(db - 2 * TTZ)));
+#pragma unroll
+        for (int j = 2; j <= R; ++j)
+          dyz = fma2(bcast(a.w1[j]), sub2(*reinterpret_cast<const f2*>(db + 2 * j * TTZ),
+                                          *reinterpret_cast<const f2*>(db - 2 * j * TTZ)), dyz);
+        gq[R + u] = fma2(bcast(st[G::O_IN + 2 * G::TILE + town]), dyz, gq[R + u]);
+      }
+      // release the stage (every read of it is above)
+      __syncwarp();
+      if (leader && mbar_arrive_last(&empty[slot])) {
+        mbar_wait(&empty[slot], phase);
+        if (p + G::NS < nplanes) issue(p + G::NS, slot);
+      }
+      if (++slot == G::NS) {
+        slot = 0;
+        phase ^= 1u;
       }
     }
 #pragma unroll
