@@ -311,7 +311,7 @@ def fp64_leg(dev, cfg, hbm, final32):
     err = float(torch.linalg.vector_norm(final32.double() - ref) / torch.linalg.vector_norm(ref))
     return {"workload": f"acoustic order {cfg.order}, {tuple(cfg.dims)}, {cfg.n_t} steps, float64",
             "gpts_per_s": round(g, 2), "ms_per_sim": round(ms, 3), "bytes_per_point": 32,
-            "frac_hbm": round(g * 32 / hbm, 4), "kernel": f"a64_stream<R={cfg.order // 2}>",
+            "frac_hbm": round(g * 32 / hbm, 4), "kernel": f"a64_queue<R={cfg.order // 2}> (AUTO)",
             "f32_rel_l2_vs_f64": err}
 
 
