@@ -2,7 +2,7 @@
 
 Re-exports the reference's kernel API (/root/reference/pkg/src/fdroof/
 __init__.py:63-74: BenchResult, KernelConfig, Source, StabilityWarning,
-Wavefield, dump_wavefield, max_stable_dt, run_benchmark, step) backed by the
+Wavefield, dump_wavefield, max_stable_dt, oracle_step, run_benchmark, step) backed by the
 sm_100a library libb200fd.so, plus the extensions the BASELINE configs need.
 """
 
@@ -23,6 +23,7 @@ from .kernel import (
     load_traces,
     load_wavefield,
     max_stable_dt,
+    oracle_step,
     run,
     run_benchmark,
     step,

@@ -789,6 +789,47 @@ __global__ void div64_selftest_kernel(long long n, double m_lo, double m_hi, uns
   atomicAdd(fast, nf);
 }
 
+
+// ------------------------------------------------- oracle_step (float64)
+// The reference's independent verification step, kernel.py:225-254: the
+// update as an explicit float64 convolution over the star stencil's points
+// in stencil_geometry("star") order (stencils.py:161-179: the centre with
+// weight 3 w0, then for j = 1..r and sign +/-: x, y, z), accumulated from
+// acc = 0 with one rounding per product and per sum (numpy, no FMA);
+// upd = (2 c - prev) + (coef acc) / m in float64; one rounding to float32
+// into the scratch level; the on-grid source added to the new value in
+// float32 (kernel.py:167-173).  One thread per interior point.
+__global__ void __launch_bounds__(256) conv64_step(const float* cur, const float* prev, float* out,
+                                                   const float* m, double m_scalar, int nx, int ny,
+                                                   int nz, int pitch_y, long long pitch_x, int r,
+                                                   const double* __restrict__ w, double coef,
+                                                   int sx, int sy, int sz, float q) {
+  const int z = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  const int x = blockIdx.z;
+  if (z >= nz) return;
+  const size_t p = (size_t)x * pitch_x + (size_t)y * pitch_y + z;
+  auto at = [&](int xx, int yy, int zz) -> double {
+    const bool in = (unsigned)xx < (unsigned)nx && (unsigned)yy < (unsigned)ny && (unsigned)zz < (unsigned)nz;
+    return in ? (double)cur[(size_t)xx * pitch_x + (size_t)yy * pitch_y + zz] : 0.0;
+  };
+  const double c = (double)cur[p];
+  double acc = __dadd_rn(0.0, __dmul_rn(w[0], c));
+  for (int j = 1; j <= r; ++j) {
+    for (int sgn = 1; sgn >= -1; sgn -= 2) {
+      const int o = sgn * j;
+      acc = __dadd_rn(acc, __dmul_rn(w[j], at(x + o, y, z)));
+      acc = __dadd_rn(acc, __dmul_rn(w[j], at(x, y + o, z)));
+      acc = __dadd_rn(acc, __dmul_rn(w[j], at(x, y, z + o)));
+    }
+  }
+  const double mm = m ? (double)m[p] : m_scalar;
+  const double upd = __dadd_rn(__dsub_rn(__dmul_rn(2.0, c), (double)prev[p]),
+                               __ddiv_rn(__dmul_rn(coef, acc), mm));
+  float v = __double2float_rn(upd);
+  if (x == sx && y == sy && z == sz) v = __fadd_rn(v, q);
+  out[p] = v;
+}
 }  // namespace fdr64
 
 extern "C" {
@@ -814,6 +855,44 @@ int64_t fdr_selftest_division64(int64_t n, double m_lo, double m_hi, uint32_t se
   return (int64_t)h[0];
 }
 
+
+int fdr_acoustic_oracle_step(const fdr_acoustic_args* a, const double* weights64, double coef64,
+                             double m_scalar64, void* stream) {
+  using fdr64::cuda_fail;
+  using fdr64::fail;
+  if (!a || a->abi_version != FDR_ABI_VERSION) return fail(FDR_EINVAL, "ABI version mismatch");
+  if (a->order < 2 || a->order > 2 * FDR_MAX_RADIUS || a->order % 2)
+    return fail(FDR_EINVAL, "order must be even in 2..%d", 2 * FDR_MAX_RADIUS);
+  if (a->nx < 1 || a->ny < 1 || a->nz < 1 || a->pitch_y < a->nz ||
+      a->pitch_x < (int64_t)a->ny * a->pitch_y || a->ny > 65535 || a->nx > 65535)
+    return fail(FDR_EINVAL, "bad extents or pitches");
+  if (!a->levels[0] || !a->levels[1] || !a->levels[2] || !weights64)
+    return fail(FDR_EINVAL, "null level or weight pointer");
+  if (a->m_mode == FDR_M_GRID && !a->m) return fail(FDR_EINVAL, "m_mode grid needs m");
+  if (a->src_w || a->rec_w) return fail(FDR_EINVAL, "oracle_step takes an on-grid source only");
+  const int r = a->order / 2;
+  double* dw = nullptr;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMallocAsync(&dw, sizeof(double) * (r + 1), st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  e = cudaMemcpyAsync(dw, weights64, sizeof(double) * (r + 1), cudaMemcpyHostToDevice, st);
+  const bool inject = a->src_x >= 0 && a->series && a->it0 < a->n_series;
+  float q = 0.0f;
+  if (e == cudaSuccess && inject)
+    e = cudaMemcpyAsync(&q, a->series + a->it0, sizeof(float), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // q is read on the host
+  if (e == cudaSuccess) {
+    dim3 grid((a->nz + 255) / 256, a->ny, a->nx);
+    fdr64::conv64_step<<<grid, 256, 0, st>>>(
+        a->levels[2], a->levels[1], a->levels[0], a->m_mode == FDR_M_GRID ? a->m : nullptr,
+        a->m_mode == FDR_M_NONE ? 1.0 : m_scalar64, a->nx, a->ny, a->nz, a->pitch_y, a->pitch_x,
+        r, dw, coef64, inject ? a->src_x : -1, a->src_y, a->src_z, q);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(dw, st);
+  if (e != cudaSuccess) return cuda_fail(e, "oracle_step");
+  return FDR_OK;
+}
 
 size_t fdr_acoustic64_args_size(void) { return sizeof(fdr_acoustic64_args); }
 

@@ -612,6 +612,53 @@ def step(fld: Wavefield, cfg: KernelConfig, slabs: int = 1) -> Wavefield:
     return run(fld, cfg, 1)
 
 
+def oracle_step(fld: Wavefield, cfg: KernelConfig) -> Wavefield:
+    """Mirror of fdroof.kernel.oracle_step (kernel.py:225-254) on the GPU.
+
+    The reference's independent check of `step`: the star-stencil convolution
+    accumulated in float64 in stencil_geometry("star") order (stencils.py:
+    161-179), the update (2c - prev) + (coef acc)/m in float64, one rounding
+    to float32, then the rotation and the source (kernel.py:219-221).  The
+    reference caps the grid at 32^3 for CPU time; this one takes any grid.
+    Like the reference it knows no sponge, receivers or off-grid source.
+    """
+    _check_match(fld, cfg)
+    if (cfg.sponge is not None or cfg.receivers is not None
+            or isinstance(cfg.source, OffGridSource)):
+        raise ValidationError("oracle_step mirrors the reference: on-grid source only, "
+                              "no sponge or receivers")
+    torch = _torch()
+    if fld.grids[0].dtype != torch.float32:
+        raise ValidationError("oracle_step takes a float32 wavefield")
+    lib = _lib.load()
+    dev = fld.device
+    pitch_y = int(fld.grids[0].shape[2])
+    pitch_x = int(fld.grids[0].shape[1]) * pitch_y
+    plan = _plan(cfg, dev, pitch_y)
+    if plan.m_grid is not None and tuple(plan.m_grid.shape) != tuple(fld.grids[0].shape):
+        plan = _DevicePlan(cfg, dev, pitch_y)
+        cfg._device_plan = plan
+    args = _lib.AcousticArgs()
+    _fill_args(args, cfg, plan, fld.dims, pitch_y, pitch_x, fld.it, 1, _lib.VARIANT_AUTO)
+    args.m = _ptr(plan.m_grid)
+    args.series = _ptr(plan.series)
+    for i in range(3):
+        args.levels[i] = fld.grids[i].data_ptr()
+    r = cfg.order // 2
+    w = second_derivative_weights(cfg.order)  # exact rationals, as fd_weights
+    w64 = (ctypes.c_double * (r + 1))(float(3 * w[r]), *(float(w[r + j]) for j in range(1, r + 1)))
+    coef = float(cfg.dt) ** 2 / float(cfg.h) ** 2  # kernel.py:246
+    m_scalar = float(cfg.m) if np.isscalar(cfg.m) else 1.0
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        _lib.check(lib.fdr_acoustic_oracle_step(ctypes.byref(args), w64, coef, m_scalar,
+                                                ctypes.c_void_p(stream)))
+    scratch, prev, cur = fld.grids
+    fld.grids = [prev, cur, scratch]
+    fld.it += 1
+    return fld
+
+
 @dataclass(frozen=True)
 class BenchResult:
     """Mirror of fdroof.kernel.BenchResult (kernel.py:257-263) plus GPts/s."""
