@@ -575,7 +575,11 @@ struct QGeoE {
   static constexpr int O_F = O_Z + NZB * ZBOX;
   static constexpr int O_C = O_F + NF * FBOX;
   static constexpr int STAGE = O_C + NC * TILE;
+#ifdef FDR_EL_NS
+  static constexpr int NS = FDR_EL_NS;
+#else
   static constexpr int NS = 3;
+#endif
   static constexpr int QD = 2 * R + 1;
   static constexpr int U = R <= 2 ? QD : 2;
   static constexpr int NWARPS = QN / 32;
@@ -657,7 +661,10 @@ FDR_DEV void stg2cs(float* p, float2 v) {
 }
 
 template <int R, int PASS, bool SPONGE>
-__global__ void __launch_bounds__(QN, 2) el_queue(const __grid_constant__ ElQMaps maps, const ElStep a) {
+#ifndef FDR_EL_MINB
+#define FDR_EL_MINB 2
+#endif
+__global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constant__ ElQMaps maps, const ElStep a) {
   using G = QGeoE<R, PASS>;
   constexpr int LZ = G::LZ;
   extern __shared__ __align__(128) float smem[];
