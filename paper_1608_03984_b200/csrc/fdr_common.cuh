@@ -58,8 +58,24 @@ FDR_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+// try_wait suspends the warp until the phase completes or a time limit
+// passes; every expiry costs a SYNCS + BRA issue slot in the spin loop.  A
+// suspend-time hint (ns, FDR_MBAR_SUSPEND_NS; 0 = the hardware default)
+// lengthens the sleep so waiting warps spin less.
+#ifndef FDR_MBAR_SUSPEND_NS
+#define FDR_MBAR_SUSPEND_NS 0
+#endif
 FDR_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
+#if FDR_MBAR_SUSPEND_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
+      "@!done bra WAIT_%=;\n}" ::"r"(addr),
+      "r"(parity), "r"((uint32_t)FDR_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred done;\n"
       "WAIT_%=:\n\t"
@@ -67,6 +83,7 @@ FDR_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!done bra WAIT_%=;\n}" ::"r"(addr),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // 3D TMA tile load global -> shared, completing on `bar` (complete_tx bytes).
