@@ -248,7 +248,11 @@ struct QG64 {
   static constexpr int STAGE = OFF_M + TILE;
   static constexpr int NS = 4;
   static constexpr int QD = 2 * R + 1;
+#ifdef FDR_A64_U
+  static constexpr int U = FDR_A64_U;
+#else
   static constexpr int U = R <= 2 ? QD : (R >= 7 ? 1 : 2);
+#endif
   static constexpr int NQ = 1 + LZ;  // double2 loads of the own z-row window
   static constexpr int NWARPS = QNT / 32;
   static constexpr size_t SMEM = size_t(NS) * STAGE * 8 + 2 * NS * 8;

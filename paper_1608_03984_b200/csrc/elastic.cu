@@ -581,7 +581,11 @@ struct QGeoE {
   static constexpr int NS = 3;
 #endif
   static constexpr int QD = 2 * R + 1;
+#ifdef FDR_ELQ_U
+  static constexpr int U = FDR_ELQ_U;
+#else
   static constexpr int U = R <= 2 ? QD : 2;
+#endif
   static constexpr int NWARPS = QN / 32;
   static constexpr size_t SMEM = size_t(NS) * STAGE * 4 + 2 * NS * 8;
   static constexpr uint32_t WIN_BYTES = 3 * TILE * 4;
