@@ -279,16 +279,26 @@ A64_DEV bool arrive_is_last(uint64_t* bar) {
 // per division early in a run).  The float32 path's scaled scheme, in double:
 // s' = s 2^600 (exact, subnormals included); r = 1/m from MUFU.RCP64H and two
 // Newton steps; q = s' r plus one exact-remainder correction (correctly
-// rounded while q is normal and nothing overflows); y = q 2^-600 is kept when
-// the downscale is exact (q - y 2^600 == +0); anything else (subnormal
-// quotients, overflow, inf/NaN, m outside the normal range) takes __ddiv_rn.
-// fdr_selftest_division64 checks the bits against __ddiv_rn.
+// rounded while q is normal and nothing overflows); y = q 2^-600.  The
+// downscale is exact unless y is subnormal; then d = q - y 2^600 (exact) is
+// the rounding error, |d| <= 2^-475 (half a subnormal ulp, scaled).  y is the
+// correctly rounded quotient unless q 2^-600 sat exactly on a midpoint of the
+// subnormal grid (|d| = 2^-475): there the double rounding may have gone the
+// wrong way, and the sign of the exact remainder e = s' - m q (Q - q has the
+// sign of e) decides: when e and d have the same sign the true quotient lies
+// past the midpoint, and y moves one subnormal ulp toward q.  Anything else
+// (overflow, inf/NaN: d is NaN; m outside [2^-500, 2^500], or below 2^-400
+// at a midpoint) takes __ddiv_rn.
+// Before the subnormal handling every subnormal quotient took __ddiv_rn,
+// whose slow path the float64 precursor ahead of a wavefront hits in bulk.
+// fdr_selftest_division64 checks the bits against __ddiv_rn (midpoints
+// included, seed bit 31).
 A64_DEV double rcp_approx64(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
   return r;
 }
-A64_DEV double ddiv_scaled(double s, double m, bool* fast) {
+A64_DEV double ddiv_scaled(double s, double m, bool* fast, bool* mid = nullptr) {
   const double sp = __dmul_rn(s, 0x1p600);
   double r = rcp_approx64(m);
   r = __fma_rn(r, __fma_rn(-m, r, 1.0), r);
@@ -297,9 +307,16 @@ A64_DEV double ddiv_scaled(double s, double m, bool* fast) {
   const double q = __fma_rn(r, __fma_rn(-m, q0, sp), q0);
   // m > 0 on the fast path, so the quotient carries the sign of s; this only
   // changes s = -0 (the remainder step returns +0 there, IEEE gives -0)
-  const double y = copysign(__dmul_rn(q, 0x1p-600), s);
-  const unsigned long long d = __double_as_longlong(__fma_rn(y, -0x1p600, q));
-  *fast = d == 0ull && m >= 0x1p-500 && m <= 0x1p500;
+  double y = copysign(__dmul_rn(q, 0x1p-600), s);
+  const double d = __fma_rn(y, -0x1p600, q);
+  const double ad = fabs(d);
+  // NaN d fails; the midpoint correction needs an exact remainder (m >= 2^-400)
+  *fast = ad <= 0x1p-475 && m >= (ad == 0x1p-475 ? 0x1p-400 : 0x1p-500) && m <= 0x1p500;
+  if (ad == 0x1p-475) {  // exact midpoint of the subnormal grid (rare)
+    const double e = __fma_rn(-m, q, sp);  // exact: q correctly rounded, m >= 2^-400
+    if (e != 0.0 && ((e > 0.0) == (d > 0.0))) y = __dadd_rn(y, __dmul_rn(d, 0x1p-599));
+    if (mid) *mid = true;
+  }
   return y;
 }
 // Out of line on purpose: inline, the compiler if-converts the select and
@@ -760,7 +777,9 @@ __device__ __forceinline__ uint32_t hmix(uint32_t x) {
 // ddiv_exact vs __ddiv_rn on n hashed pairs: |s| log-uniform over
 // [2^-1080, 2^520] (random mantissas, both signs, zeros, subnormals, edge
 // values), m log-uniform over [m_lo, m_hi]; counts mismatching bits and the
-// pairs that took the fast path.
+// pairs that took the fast path.  With seed bit 31 set every pair is a
+// constructed subnormal-midpoint candidate and the second count is the pairs
+// the fast path resolved through its midpoint correction.
 __global__ void div64_selftest_kernel(long long n, double m_lo, double m_hi, unsigned seed,
                                       unsigned long long* bad, unsigned long long* fast) {
   unsigned long long nb = 0, nf = 0;
@@ -783,9 +802,19 @@ __global__ void div64_selftest_kernel(long long n, double m_lo, double m_hi, uns
     m = __longlong_as_double((__double_as_longlong(m) & 0xfff0000000000000ull) |
                              (((unsigned long long)hmix(h4) << 21 ^ h1) & 0x000fffffffffffffull));
     m = fmin(fmax(m, m_lo), m_hi);
-    bool f;
-    const double y = ddiv_scaled(s, m, &f);
-    nf += f;
+    if (seed & 0x80000000u) {
+      // midpoint candidates: s = j 2^-1074 (exact subnormal) and m = RN(2j / k)
+      // with k odd (up to 2^40), so s'/m is within a relative 2^-53 of the
+      // subnormal-grid midpoint k 2^-1075 (scaled: k 2^-475) and q often
+      // rounds onto it exactly; the sign of the remainder then varies
+      const double k = (double)((((unsigned long long)h4 << 8) ^ h1) & 0xffffffffffull) * 2.0 + 1.0;
+      const double j = fmin(fmax(floor(k * m * 0.5), 1.0), 4503599627370495.0);
+      s = (h2 & 1u ? -j : j) * 0x1p-1074;
+      m = fmin(fmax(__ddiv_rn(2.0 * j, k), m_lo), m_hi);
+    }
+    bool f, mid = false;
+    const double y = ddiv_scaled(s, m, &f, &mid);
+    nf += (seed & 0x80000000u) ? (f && mid) : f;
     const double q = f ? y : __ddiv_rn(s, m);
     if (__double_as_longlong(q) != __double_as_longlong(__ddiv_rn(s, m))) ++nb;
   }

@@ -176,3 +176,18 @@ def test_gpu_f64_scaled_division_matches_ieee(B, m_lo, m_hi):
     bad, n_fast = selftest_division64(n, m_lo, m_hi, seed=7)
     assert bad == 0
     assert n_fast > n // 8
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m_lo,m_hi", [(4.9e-8, 4.5e-7), (0.5, 2.0), (2.0 ** -60, 2.0 ** 40)])
+def test_gpu_f64_division_subnormal_midpoints(B, m_lo, m_hi):
+    """Subnormal quotients stay on the fast path; the double-rounding hazard
+    (the scaled quotient exactly on a midpoint of the subnormal grid) is
+    resolved by the remainder sign.  Constructed midpoint candidates (seed
+    bit 31) against __ddiv_rn bit for bit, with the correction branch taken."""
+    from paper_1608_03984_b200.kernel import selftest_division64
+
+    n = 1 << 24
+    bad, n_mid = selftest_division64(n, m_lo, m_hi, seed=0x80000000 | 11)
+    assert bad == 0
+    assert n_mid > n // 64

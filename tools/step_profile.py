@@ -21,6 +21,7 @@ def main():
     p.add_argument("--random", action="store_true")
     p.add_argument("--m1", action="store_true", help="scalar m = 1 (no division)")
     p.add_argument("--count", action="store_true", help="report slow-path quads (instrumented lib)")
+    p.add_argument("--f64", action="store_true", help="float64 levels (a64 kernels)")
     a = p.parse_args()
     import numpy as np
     import torch
@@ -43,7 +44,7 @@ def main():
         slow = _lib.load().fdr_debug_slow_quads
         slow.restype = ctypes.c_ulonglong
         slow.argtypes = [ctypes.c_int]
-    fld = B.Wavefield.allocate(cfg.dims, cfg.halo)
+    fld = B.Wavefield.allocate(cfg.dims, cfg.halo, dtype=torch.float64 if a.f64 else torch.float32)
     npts = float(np.prod(cfg.dims))
     B.run(fld, cfg, 1)
     fld.it = 0
@@ -51,8 +52,9 @@ def main():
         g.zero_()
     if a.random:
         rng = np.random.default_rng(1)
-        fld.set_interior(2, rng.standard_normal(cfg.dims, dtype=np.float32))
-        fld.set_interior(1, rng.standard_normal(cfg.dims, dtype=np.float32))
+        dt = np.float64 if a.f64 else np.float32
+        fld.set_interior(2, rng.standard_normal(cfg.dims).astype(dt))
+        fld.set_interior(1, rng.standard_normal(cfg.dims).astype(dt))
     done = 0
     while done < a.nt:
         n = min(a.seg, a.nt - done)
@@ -65,11 +67,12 @@ def main():
         e.synchronize()
         ms = s.elapsed_time(e) / n
         u = fld.interior().abs()
-        tiny = 2.0 ** -100
+        tiny = 2.0 ** (-900 if a.f64 else -100)
+        sub = 2.0 ** (-1022 if a.f64 else -126)
         st = {"steps": f"{done}-{done + n}", "ms_per_step": round(ms, 4),
               "gpts": round(npts / ms / 1e6, 1),
               "zero": round(float((u == 0).float().mean()), 4),
-              "subnormal": round(float(((u > 0) & (u < 2.0 ** -126)).float().mean()), 4),
+              "subnormal": round(float(((u > 0) & (u < sub)).float().mean()), 4),
               "lt_2m100": round(float(((u > 0) & (u < tiny)).float().mean()), 4),
               "max": float(u.max())}
         if slow is not None:
