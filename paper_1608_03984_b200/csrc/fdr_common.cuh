@@ -65,8 +65,7 @@ FDR_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 #ifndef FDR_MBAR_SUSPEND_NS
 #define FDR_MBAR_SUSPEND_NS 0
 #endif
-FDR_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
+FDR_DEV void mbar_wait_a(uint32_t addr, uint32_t parity) {
 #if FDR_MBAR_SUSPEND_NS > 0
   asm volatile(
       "{\n\t.reg .pred done;\n"
@@ -85,6 +84,7 @@ FDR_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 #endif
 }
+FDR_DEV void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_a(smem_u32(bar), parity); }
 
 // 3D TMA tile load global -> shared, completing on `bar` (complete_tx bytes).
 // Coordinates are element indices (z, y, x) and may be negative / beyond the
@@ -120,6 +120,25 @@ FDR_DEV void stg_stream(float* p, float4 v) {
 }
 
 FDR_DEV float4 lds128(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// 16-byte shared load from a 32-bit shared-window address.  Volatile: the
+// loads must stay after the stage's mbarrier wait (also a volatile asm).
+FDR_DEV float4 lds128a(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+
+// One lane of a converged warp (elect.sync): no thread-index read.
+FDR_DEV bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(e));
+  return e != 0u;
+}
 
 // Register copy pinned to the ALU pipe.  ptxas emits plain copies as
 // IMAD.MOV (FMA pipe, 2 cycles per warp instruction) about half the time;
