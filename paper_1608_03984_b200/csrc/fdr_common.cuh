@@ -131,6 +131,21 @@ FDR_DEV float4 lds128a(uint32_t a) {
   return v;
 }
 
+FDR_DEV float lds32a(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
+FDR_DEV unsigned long long lds64a(uint32_t a) {
+  unsigned long long v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+FDR_DEV void sts64a(uint32_t a, unsigned long long v) {
+  asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
 // One lane of a converged warp (elect.sync): no thread-index read.
 FDR_DEV bool elect_one() {
   uint32_t e;

@@ -216,17 +216,19 @@ struct TTIMaps {
   CUtensorMap prm[9];         // k a b cxx cyy czz cxy cyz cxz, tiles
 };
 
-FDR_DEV void mbar_arrive_t(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+FDR_DEV void mbar_arrive_ta(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+FDR_DEV void mbar_arrive_t(uint64_t* bar) { mbar_arrive_ta(smem_u32(bar)); }
 
-FDR_DEV bool mbar_arrive_last(uint64_t* bar) {
+FDR_DEV bool mbar_arrive_last_a(uint32_t bar) {
   uint64_t state;
   uint32_t pending;
-  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(state) : "r"(smem_u32(bar)) : "memory");
+  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(state) : "r"(bar) : "memory");
   asm volatile("mbarrier.pending_count.b64 %0, %1;" : "=r"(pending) : "l"(state));
   return pending == 1;
 }
+FDR_DEV bool mbar_arrive_last(uint64_t* bar) { return mbar_arrive_last_a(smem_u32(bar)); }
 
 template <int R>
 FDR_DEV float d1_row(const float* row, const float* w1) {  // D1 along z at row[0]
@@ -457,6 +459,23 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_stream(const __grid_constant__
 // updates are per field (scalar, in the oracle's order).
 FDR_DEV f2 bcast(float w) { return pk(w, w); }
 FDR_DEV f2 ldpr(const float* p, const float* r, int off) { return pk(p[off], r[off]); }
+// The same from a 32-bit shared address of the p element; the r box is `dr`
+// bytes further.
+FDR_DEV f2 ldpra(uint32_t ap, uint32_t dr, int off) {
+  return pk(lds32a(ap + 4 * off), lds32a(ap + dr + 4 * off));
+}
+template <int R>
+FDR_DEV f2 d1_row2a(uint32_t hp, uint32_t dr, const float* w1) {  // D1z, both fields
+  f2 d = mul2(bcast(w1[1]), sub2(ldpra(hp, dr, 1), ldpra(hp, dr, -1)));
+#pragma unroll
+  for (int j = 2; j <= R; ++j) d = fma2(bcast(w1[j]), sub2(ldpra(hp, dr, j), ldpra(hp, dr, -j)), d);
+  return d;
+}
+#ifdef FDR_TTI_CARRY
+constexpr bool TTI_CARRY = FDR_TTI_CARRY != 0;
+#else
+constexpr bool TTI_CARRY = true;
+#endif
 
 template <int R>
 FDR_DEV f2 d1_row2(const float* hp, const float* hr, const float* w1) {  // D1z, both fields
@@ -551,58 +570,76 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
 
   int slot = 0;
   uint32_t phase = 0;
+  // 32-bit shared addresses of this thread's elements in stage `slot`,
+  // carried across planes so ptxas cannot rematerialise them from the thread
+  // index every plane (as in acoustic_queue)
+  constexpr bool CA = TTI_CARRY;
+  constexpr uint32_t SB = G::STAGE * 4u, DR = (G::O_BR - G::O_BP) * 4u;
+  const int hr0 = hrow >= 0 ? hrow : 0;
+  uint32_t ab = smem_u32(smem + G::O_BP + bown), at = smem_u32(smem + town);
+  uint32_t adz = smem_u32(smem + G::O_DZP + 2 * ((ty + R) * TTZ + tz));
+  uint32_t ah = smem_u32(smem + G::O_BP + hr0 * G::BZ + G::LZ + tz);
+  uint32_t ahdz = smem_u32(smem + G::O_DZP + 2 * (hr0 * TTZ + tz));
+  uint32_t af = smem_u32(full);  // full[slot]; empty[] and dzrdy[] follow
 #pragma unroll 1
   for (int p0 = 0; p0 < nplanes; p0 += G::U) {
 #pragma unroll
     for (int u = 0; u < G::U; ++u) {
       const int p = p0 + u;
       if (p >= nplanes) break;
-      mbar_wait(&full[slot], phase);
+      if (CA) mbar_wait_a(af, phase); else mbar_wait(&full[slot], phase);
       float* st = smem + slot * G::STAGE;
+      auto lp = [&](int off) { return CA ? ldpra(ab, DR, off) : ldpr(st + G::O_BP + bown, st + G::O_BR + bown, off); };
+      auto lt = [&](int off) { return CA ? lds32a(at + 4 * off) : st[town + off]; };
       // ---- in-plane work on the newest plane, both fields packed
-      const float* cp = st + G::O_BP + bown;
-      const float* cr = st + G::O_BR + bown;
-      const f2 uo = ldpr(cp, cr, 0);
-      f2 dy1 = mul2(bcast(a.w1[1]), sub2(ldpr(cp, cr, G::BZ), ldpr(cp, cr, -G::BZ)));
+      const f2 uo = lp(0);
+      f2 dy1 = mul2(bcast(a.w1[1]), sub2(lp(G::BZ), lp(-G::BZ)));
       f2 dyy = mul2(bcast(a.w2[0]), uo);
 #pragma unroll
       for (int j = 1; j <= R; ++j) {
-        const f2 up = ldpr(cp, cr, j * G::BZ), um = ldpr(cp, cr, -j * G::BZ);
+        const f2 up = lp(j * G::BZ), um = lp(-j * G::BZ);
         if (j >= 2) dy1 = fma2(bcast(a.w1[j]), sub2(up, um), dy1);
         dyy = fma2(bcast(a.w2[j]), add2(up, um), dyy);
       }
-      f2 dz1 = mul2(bcast(a.w1[1]), sub2(ldpr(cp, cr, 1), ldpr(cp, cr, -1)));
+      f2 dz1 = mul2(bcast(a.w1[1]), sub2(lp(1), lp(-1)));
       f2 dzz = mul2(bcast(a.w2[0]), uo);
 #pragma unroll
       for (int j = 1; j <= R; ++j) {
-        const f2 up = ldpr(cp, cr, j), um = ldpr(cp, cr, -j);
+        const f2 up = lp(j), um = lp(-j);
         if (j >= 2) dz1 = fma2(bcast(a.w1[j]), sub2(up, um), dz1);
         dzz = fma2(bcast(a.w2[j]), add2(up, um), dzz);
       }
       float* dzb = st + G::O_DZP;  // interleaved (p, r) D1z rows, 2 * BY * TTZ floats
-      *reinterpret_cast<f2*>(dzb + 2 * ((ty + R) * TTZ + tz)) = dz1;
-      if (hrow >= 0)
-        *reinterpret_cast<f2*>(dzb + 2 * (hrow * TTZ + tz)) =
-            d1_row2<R>(st + G::O_BP + hrow * G::BZ + G::LZ + tz, st + G::O_BR + hrow * G::BZ + G::LZ + tz, a.w1);
+      if (CA) {
+        sts64a(adz, dz1);
+        if (hrow >= 0) sts64a(ahdz, d1_row2a<R>(ah, DR, a.w1));
+      } else {
+        *reinterpret_cast<f2*>(dzb + 2 * ((ty + R) * TTZ + tz)) = dz1;
+        if (hrow >= 0)
+          *reinterpret_cast<f2*>(dzb + 2 * (hrow * TTZ + tz)) =
+              d1_row2<R>(st + G::O_BP + hrow * G::BZ + G::LZ + tz, st + G::O_BR + hrow * G::BZ + G::LZ + tz, a.w1);
+      }
       qu[2 * R + u] = uo;
       qy[2 * R + u] = dy1;
       qz[2 * R + u] = dz1;
       pl[R + u] = __fadd_rn(lo(dyy), lo(dzz));
       // gin = fma(cyz, dyz, fma(czz, dzz, cyy dyy)): the dyz term follows the barrier
-      gq[R + u] = fma2(bcast(st[G::O_IN + 1 * G::TILE + town]), dzz, mul2(bcast(st[G::O_IN + town]), dyy));
+      gq[R + u] = fma2(bcast(lt(G::O_IN + 1 * G::TILE)), dzz, mul2(bcast(lt(G::O_IN)), dyy));
       // Split barrier: announce this warp's D1z rows, update the plane R
       // behind (which needs no D1z row of this plane), then wait for every
       // warp's rows.  The warps' skew is absorbed by useful work instead of a
       // __syncthreads.
       __syncwarp();
-      if (leader) mbar_arrive_t(&dzrdy[slot]);
+      if (CA ? elect_one() : leader) {
+        if (CA) mbar_arrive_ta(af + 16u * G::NS); else mbar_arrive_t(&dzrdy[slot]);
+      }
       // ---- the plane R behind: x derivatives and the update
       const int k = p - 2 * R;
       if (k >= 0) {
-        const float* cen = st + G::O_CEN + town;
-        const float vk = cen[0], va = cen[G::TILE], vb = cen[2 * G::TILE];
-        const float cxx = cen[3 * G::TILE], cxy = cen[4 * G::TILE], cxz = cen[5 * G::TILE];
-        const float ppv = cen[6 * G::TILE], rpv = cen[7 * G::TILE];
+        const float vk = lt(G::O_CEN), va = lt(G::O_CEN + G::TILE), vb = lt(G::O_CEN + 2 * G::TILE);
+        const float cxx = lt(G::O_CEN + 3 * G::TILE), cxy = lt(G::O_CEN + 4 * G::TILE);
+        const float cxz = lt(G::O_CEN + 5 * G::TILE);
+        const float ppv = lt(G::O_CEN + 6 * G::TILE), rpv = lt(G::O_CEN + 7 * G::TILE);
         const int c = u + R;
         f2 dxx = mul2(bcast(a.w2[0]), qu[c]);
         f2 dxy = mul2(bcast(a.w1[1]), sub2(qy[c + 1], qy[c - 1]));
@@ -637,26 +674,35 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
           a.rn[o] = rn;
         }
       }
-      mbar_wait(&dzrdy[slot], phase);  // the D1z rows are complete
+      // the D1z rows are complete
+      if (CA) mbar_wait_a(af + 16u * G::NS, phase); else mbar_wait(&dzrdy[slot], phase);
       {
         const float* db = dzb + 2 * ((ty + R) * TTZ + tz);
-        f2 dyz = mul2(bcast(a.w1[1]), sub2(*reinterpret_cast<const f2*>(db + 2 * TTZ),
-                                           *reinterpret_cast<const f2*>(db - 2 * TTZ)));
+        auto ldz = [&](int rows) {
+          return CA ? lds64a(adz + 8 * rows * TTZ) : *reinterpret_cast<const f2*>(db + 2 * rows * TTZ);
+        };
+        f2 dyz = mul2(bcast(a.w1[1]), sub2(ldz(1), ldz(-1)));
 #pragma unroll
-        for (int j = 2; j <= R; ++j)
-          dyz = fma2(bcast(a.w1[j]), sub2(*reinterpret_cast<const f2*>(db + 2 * j * TTZ),
-                                          *reinterpret_cast<const f2*>(db - 2 * j * TTZ)), dyz);
-        gq[R + u] = fma2(bcast(st[G::O_IN + 2 * G::TILE + town]), dyz, gq[R + u]);
+        for (int j = 2; j <= R; ++j) dyz = fma2(bcast(a.w1[j]), sub2(ldz(j), ldz(-j)), dyz);
+        gq[R + u] = fma2(bcast(lt(G::O_IN + 2 * G::TILE)), dyz, gq[R + u]);
       }
       // release the stage (every read of it is above)
       __syncwarp();
-      if (leader && mbar_arrive_last(&empty[slot])) {
-        mbar_wait(&empty[slot], phase);
+      if (CA ? (elect_one() && mbar_arrive_last_a(af + 8u * G::NS))
+             : (leader && mbar_arrive_last(&empty[slot]))) {
+        if (CA) mbar_wait_a(af + 8u * G::NS, phase); else mbar_wait(&empty[slot], phase);
         if (p + G::NS < nplanes) issue(p + G::NS, slot);
+      }
+      if (CA) {
+        ab += SB; at += SB; adz += SB; ah += SB; ahdz += SB; af += 8u;
       }
       if (++slot == G::NS) {
         slot = 0;
         phase ^= 1u;
+        if (CA) {
+          ab -= G::NS * SB; at -= G::NS * SB; adz -= G::NS * SB;
+          ah -= G::NS * SB; ahdz -= G::NS * SB; af -= 8u * G::NS;
+        }
       }
     }
 #pragma unroll
