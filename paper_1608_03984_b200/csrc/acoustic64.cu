@@ -259,18 +259,25 @@ struct QG64 {
 };
 
 A64_DEV double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+// from a 32-bit shared-window address (volatile: stays after the stage wait)
+A64_DEV double2 lds2a(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
 
 A64_DEV void stg2_stream(double* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
-A64_DEV bool arrive_is_last(uint64_t* bar) {
+A64_DEV bool arrive_is_last_a(uint32_t bar) {
   uint64_t state;
   uint32_t pending;
-  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(state) : "r"(fdr::smem_u32(bar)) : "memory");
+  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(state) : "r"(bar) : "memory");
   asm volatile("mbarrier.pending_count.b64 %0, %1;" : "=r"(pending) : "l"(state));
   return pending == 1;
 }
+A64_DEV bool arrive_is_last(uint64_t* bar) { return arrive_is_last_a(fdr::smem_u32(bar)); }
 
 // Correctly rounded s / m in double without __ddiv_rn's slow path for tiny
 // dividends.  In float64 the numerical precursor ahead of a wavefront decays
@@ -357,7 +364,6 @@ __global__ void __launch_bounds__(QNT, 2)
   if (xb >= xe) return;
   const int n = xe - xb;
   const int nplanes = n + 2 * R;  // stream plane p: newest x = xb - R + p
-  const bool leader = (tid & 31) == 0;
 
   auto issue = [&](int p, int sl) {
     double* st = ring + sl * G::STAGE;
@@ -391,7 +397,6 @@ __global__ void __launch_bounds__(QNT, 2)
   const bool row_ok = y < a.ny;
   const bool vec_ok = row_ok && zb + 1 < a.nz;
   const int bcen = G::OFF_BOX + (ty + R) * G::BZ + G::LZ + 2 * tz;
-  const int zrow = G::OFF_BOX + (ty + R) * G::BZ + 2 * tz;
   const int tcol = ty * QTZ + 2 * tz;
   double gyz0 = 1.0, gyz1 = 1.0, gyv = 1.0;
   if (SPONGE && row_ok) {
@@ -410,15 +415,27 @@ __global__ void __launch_bounds__(QNT, 2)
 
   int slot = 0;
   uint32_t phase = 0;
+  // own-column / own-box-row / full-barrier shared addresses of stage `slot`,
+  // carried across planes (no thread-index rematerialisation per plane, as in
+  // the float32 kernel)
+  constexpr uint32_t SB = G::STAGE * 8u;
+  uint32_t ac = fdr::smem_u32(ring + tcol), ab = fdr::smem_u32(ring + bcen);
+  uint32_t af = fdr::smem_u32(full);  // empty[slot] is 8 NS bytes further
   auto finish = [&](int p) {
     __syncwarp();
-    if (leader && arrive_is_last(&empty[slot])) {
-      mbar_wait(&empty[slot], phase);
+    if (fdr::elect_one() && arrive_is_last_a(af + 8u * G::NS)) {
+      fdr::mbar_wait_a(af + 8u * G::NS, phase);
       if (p + G::NS < nplanes) issue(p + G::NS, slot);
     }
+    ac += SB;
+    ab += SB;
+    af += 8u;
     if (++slot == G::NS) {
       slot = 0;
       phase ^= 1u;
+      ac -= G::NS * SB;
+      ab -= G::NS * SB;
+      af -= 8u * G::NS;
     }
   };
 
@@ -426,8 +443,8 @@ __global__ void __launch_bounds__(QNT, 2)
   double2 qw[2 * R + G::U];
 #pragma unroll
   for (int p = 0; p < 2 * R; ++p) {
-    mbar_wait(&full[slot], phase);
-    qw[p] = lds2(ring + slot * G::STAGE + tcol);
+    fdr::mbar_wait_a(af, phase);
+    qw[p] = lds2a(ac);
     finish(p);
   }
 
@@ -438,13 +455,12 @@ __global__ void __launch_bounds__(QNT, 2)
       const int p = p0 + u;
       if (p >= nplanes) break;
       const int k = p - 2 * R;
-      mbar_wait(&full[slot], phase);
-      const double* st = ring + slot * G::STAGE;
-      qw[ROTATE ? (2 * R + u) % G::QD : 2 * R + u] = lds2(st + tcol);
+      fdr::mbar_wait_a(af, phase);
+      qw[ROTATE ? (2 * R + u) % G::QD : 2 * R + u] = lds2a(ac);
       double zr[2 + 2 * G::LZ];
 #pragma unroll
       for (int qd = 0; qd < G::NQ; ++qd) {
-        const double2 v = lds2(st + zrow + 2 * qd);
+        const double2 v = lds2a(ab + 8u * (2 * qd - G::LZ));
         zr[2 * qd] = v.x;
         zr[2 * qd + 1] = v.y;
       }
@@ -459,8 +475,8 @@ __global__ void __launch_bounds__(QNT, 2)
       }
 #pragma unroll
       for (int j = 1; j <= R; ++j) {  // y taps from the centre box
-        const double2 pp = lds2(st + bcen + j * G::BZ);
-        const double2 mm = lds2(st + bcen - j * G::BZ);
+        const double2 pp = lds2a(ab + 8u * (j * G::BZ));
+        const double2 mm = lds2a(ab - 8u * (j * G::BZ));
         l0 = tapd(l0, a.w[j], pp.x, mm.x);
         l1 = tapd(l1, a.w[j], pp.y, mm.y);
       }
@@ -469,9 +485,9 @@ __global__ void __launch_bounds__(QNT, 2)
         l0 = tapd(l0, a.w[j], zr[G::LZ + j], zr[G::LZ - j]);
         l1 = tapd(l1, a.w[j], zr[G::LZ + 1 + j], zr[G::LZ + 1 - j]);
       }
-      const double2 pv = lds2(st + G::OFF_PREV + tcol);
+      const double2 pv = lds2a(ac + 8u * G::OFF_PREV);
       double2 mv = make_double2(1.0, 1.0);
-      if (GRID_M) mv = lds2(st + G::OFF_M + tcol);
+      if (GRID_M) mv = lds2a(ac + 8u * G::OFF_M);
       finish(p);
       double o0 = __dadd_rn(__dsub_rn(__dadd_rn(c0, c0), pv.x),
                             divide64<GRID_M>(a, __dmul_rn(a.coef, l0), mv.x));

@@ -285,13 +285,14 @@ struct ElMaps {
   CUtensorMap tile[9];  // velocity pass: sxx vx vy vz bs; stress: sxx..syz lam mu
 };
 
-FDR_DEV bool el_arrive_last(uint64_t* bar) {
+FDR_DEV bool el_arrive_last_a(uint32_t bar) {
   uint64_t state;
   uint32_t pending;
-  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(state) : "r"(smem_u32(bar)) : "memory");
+  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(state) : "r"(bar) : "memory");
   asm volatile("mbarrier.pending_count.b64 %0, %1;" : "=r"(pending) : "l"(state));
   return pending == 1;
 }
+FDR_DEV bool el_arrive_last(uint64_t* bar) { return el_arrive_last_a(smem_u32(bar)); }
 
 // staggered differences on a strided line (p points at the own element)
 template <int R>
@@ -607,17 +608,26 @@ FDR_DEV f2 f2of(float2 v) { return pk(v.x, v.y); }
 FDR_DEV float2 f2to(f2 v) { return make_float2(lo(v), hi(v)); }
 FDR_DEV f2 bcw(float c) { return pk(c, c); }
 FDR_DEV f2 ldf2(const float* p) { return *reinterpret_cast<const f2*>(p); }
+// A 32-bit shared-window address in float units of offset, so the strided
+// helpers below run on addresses the queue kernel carries across planes
+// (ptxas then cannot rematerialise them from the thread index every plane).
+struct SAddr {
+  uint32_t a;
+};
+FDR_DEV SAddr operator+(SAddr p, int off) { return {p.a + 4u * (uint32_t)off}; }
+FDR_DEV SAddr operator-(SAddr p, int off) { return {p.a - 4u * (uint32_t)off}; }
+FDR_DEV f2 ldf2(SAddr p) { return lds64a(p.a); }
 
 // p points at the own pair, s = the element stride of the differenced axis
-template <int R>
-FDR_DEV float2 pF2(const float* p, int s, const float* c) {
+template <int R, class P>
+FDR_DEV float2 pF2(P p, int s, const float* c) {
   f2 d = mul2(bcw(c[1]), sub2(ldf2(p + s), ldf2(p)));
 #pragma unroll
   for (int k = 2; k <= R; ++k) d = fma2(bcw(c[k]), sub2(ldf2(p + k * s), ldf2(p + (1 - k) * s)), d);
   return f2to(d);
 }
-template <int R>
-FDR_DEV float2 pB2(const float* p, int s, const float* c) {
+template <int R, class P>
+FDR_DEV float2 pB2(P p, int s, const float* c) {
   f2 d = mul2(bcw(c[1]), sub2(ldf2(p), ldf2(p - s)));
 #pragma unroll
   for (int k = 2; k <= R; ++k) d = fma2(bcw(c[k]), sub2(ldf2(p + (k - 1) * s), ldf2(p - k * s)), d);
@@ -664,6 +674,9 @@ FDR_DEV void stg2cs(float* p, float2 v) {
   asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
 
+#ifndef FDR_EL_CARRY_STRESS
+#define FDR_EL_CARRY_STRESS 0
+#endif
 template <int R, int PASS, bool SPONGE>
 #ifndef FDR_EL_MINB
 #define FDR_EL_MINB 2
@@ -683,7 +696,6 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
   if (xb >= xe) return;
   const int n = xe - xb;
   const int nplanes = n + 2 * R;
-  const bool leader = (tid & 31) == 0;
 
   auto issue = [&](int pl, int sl) {
     float* st = smem + sl * G::STAGE;
@@ -722,6 +734,13 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
   const int ycol = (ty + R) * QZ + 2 * tz;              // in a y-box
   const int zrow = ty * G::ZB + 2 * tz;                 // own row window start in a z-box
   const int frow = (ty + R) * G::ZB + 2 * tz;           // own row window start in a full box
+  // the same as 32-bit shared addresses in stage `slot`, carried across planes
+  // in the velocity pass; the stress pass (at the 128-register cap, where three
+  // carried addresses spill) re-forms them from the slot every plane
+  constexpr bool CA = PASS == 0 || FDR_EL_CARRY_STRESS;
+  const SAddr s0{smem_u32(smem)};
+  SAddr at_ = s0 + tcol, ay = s0 + ycol, az = s0 + zrow, afr = s0 + frow;
+  uint32_t af = smem_u32(full);  // full[slot]; empty[slot] is 8 NS bytes on
   float gy = 1.0f, gz0 = 1.0f, gz1 = 1.0f;
   if (SPONGE && row_ok) {
     gy = a.gy[y];
@@ -748,39 +767,47 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
     for (int u = 0; u < G::U; ++u) {
       const int pl = p0 + u;
       if (pl >= nplanes) break;
-      mbar_wait(&full[slot], phase);
-      const float* st = smem + slot * G::STAGE;
+      if (!CA) {
+        const SAddr sl0 = s0 + slot * G::STAGE;
+        at_ = sl0 + tcol;
+        ay = sl0 + ycol;
+        az = sl0 + zrow;
+        afr = sl0 + frow;
+        af = smem_u32(full + slot);
+      }
+      mbar_wait_a(af, phase);
+      auto ld2 = [](SAddr p) { return f2to(ldf2(p)); };
       // queue slot of the newest plane: index 2R + u of this round (plane p0 - 2R + i at i)
       const int qn = ROT ? (2 * R + u) % G::QD : 2 * R + u;
-      q0[qn] = *reinterpret_cast<const float2*>(st + G::O_WIN + tcol);
-      q1[qn] = *reinterpret_cast<const float2*>(st + G::O_WIN + G::TILE + tcol);
-      q2[qn] = *reinterpret_cast<const float2*>(st + G::O_WIN + 2 * G::TILE + tcol);
+      q0[qn] = ld2(at_ + G::O_WIN);
+      q1[qn] = ld2(at_ + (G::O_WIN + G::TILE));
+      q2[qn] = ld2(at_ + (G::O_WIN + 2 * G::TILE));
       const int k = pl - 2 * R;
       float2 out[6];
       if (k >= 0) {
         const int ci = R + u;  // queue index of the centre plane
         if (PASS == 0) {
-          const float* sxy = st + G::O_Y + ycol;
-          const float* syy = st + G::O_Y + G::YBOX + ycol;
+          const SAddr sxy = ay + G::O_Y;
+          const SAddr syy = ay + (G::O_Y + G::YBOX);
           float zw[2 + 2 * LZ], zw2[2 + 2 * LZ], fw[2 + 2 * LZ];
 #pragma unroll
           for (int i = 0; i < 1 + LZ; ++i) {
-            const float2 v = *reinterpret_cast<const float2*>(st + G::O_Z + zrow + 2 * i);
-            const float2 w = *reinterpret_cast<const float2*>(st + G::O_Z + G::ZBOX + zrow + 2 * i);
-            const float2 f = *reinterpret_cast<const float2*>(st + G::O_F + frow + 2 * i);
+            const float2 v = ld2(az + (G::O_Z + 2 * i));
+            const float2 w = ld2(az + (G::O_Z + G::ZBOX + 2 * i));
+            const float2 f = ld2(afr + (G::O_F + 2 * i));
             zw[2 * i] = v.x; zw[2 * i + 1] = v.y;
             zw2[2 * i] = w.x; zw2[2 * i + 1] = w.y;
             fw[2 * i] = f.x; fw[2 * i + 1] = f.y;
           }
-          const float* syz = st + G::O_F + frow + LZ;
+          const SAddr syz = afr + (G::O_F + LZ);
           const float2 d0 = add2f(pB2<R>(sxy, QZ, a.c), zB2<R, LZ>(zw, a.c));     // By sxy + Bz sxz
           const float2 d1 = add2f(pF2<R>(syy, QZ, a.c), zB2<R, LZ>(fw, a.c));     // Fy syy + Bz syz
           const float2 d2 = add2f(pB2<R>(syz, G::ZB, a.c), zF2<R, LZ>(zw2, a.c)); // By syz + Fz szz
-          const float* ct = st + G::O_C + tcol;
-          const float2 vx = *reinterpret_cast<const float2*>(ct);
-          const float2 vy = *reinterpret_cast<const float2*>(ct + G::TILE);
-          const float2 vz = *reinterpret_cast<const float2*>(ct + 2 * G::TILE);
-          const float2 bs = *reinterpret_cast<const float2*>(ct + 3 * G::TILE);
+          const SAddr ct = at_ + G::O_C;
+          const float2 vx = ld2(ct);
+          const float2 vy = ld2(ct + G::TILE);
+          const float2 vz = ld2(ct + 2 * G::TILE);
+          const float2 bs = ld2(ct + 3 * G::TILE);
           out[0] = fma2f(bs, add2f(d0, xF2<R, G::QD, ROT>(q0, ci, a.c)), vx);
           out[1] = fma2f(bs, add2f(d1, xB2<R, G::QD, ROT>(q1, ci, a.c)), vy);
           out[2] = fma2f(bs, add2f(d2, xB2<R, G::QD, ROT>(q2, ci, a.c)), vz);
@@ -788,26 +815,26 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
           float xw[2 + 2 * LZ], yw[2 + 2 * LZ], zw[2 + 2 * LZ];
 #pragma unroll
           for (int i = 0; i < 1 + LZ; ++i) {
-            const float2 v0 = *reinterpret_cast<const float2*>(st + G::O_F + frow + 2 * i);
-            const float2 v1 = *reinterpret_cast<const float2*>(st + G::O_F + G::FBOX + frow + 2 * i);
-            const float2 v2 = *reinterpret_cast<const float2*>(st + G::O_F + 2 * G::FBOX + frow + 2 * i);
+            const float2 v0 = ld2(afr + (G::O_F + 2 * i));
+            const float2 v1 = ld2(afr + (G::O_F + G::FBOX + 2 * i));
+            const float2 v2 = ld2(afr + (G::O_F + 2 * G::FBOX + 2 * i));
             xw[2 * i] = v0.x; xw[2 * i + 1] = v0.y;
             yw[2 * i] = v1.x; yw[2 * i + 1] = v1.y;
             zw[2 * i] = v2.x; zw[2 * i + 1] = v2.y;
           }
-          const float* vxb = st + G::O_F + frow + LZ;
-          const float* vyb = vxb + G::FBOX;
-          const float* vzb = vxb + 2 * G::FBOX;
+          const SAddr vxb = afr + (G::O_F + LZ);
+          const SAddr vyb = vxb + G::FBOX;
+          const SAddr vzb = vxb + 2 * G::FBOX;
           const float2 ey = pB2<R>(vyb, G::ZB, a.c);
           const float2 ez = zB2<R, LZ>(zw, a.c);
           const float2 fyvx = pF2<R>(vxb, G::ZB, a.c);
           const float2 fzvx = zF2<R, LZ>(xw, a.c);
           const float2 d4 = add2f(zF2<R, LZ>(yw, a.c), pF2<R>(vzb, G::ZB, a.c));  // Fz vy + Fy vz
           const float2 ex = xB2<R, G::QD, ROT>(q0, ci, a.c);
-          const float* ct = st + G::O_C + tcol;
+          const SAddr ct = at_ + G::O_C;
           float2 cv[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) cv[t] = *reinterpret_cast<const float2*>(ct + t * G::TILE);
+          for (int t = 0; t < 8; ++t) cv[t] = ld2(ct + t * G::TILE);
           const float2 lam = cv[6], mu = cv[7];
           const float2 l2m = make_float2(__fmaf_rn(2.0f, mu.x, lam.x), __fmaf_rn(2.0f, mu.y, lam.y));
           out[0] = fma2f(lam, add2f(ey, ez), fma2f(l2m, ex, cv[0]));
@@ -820,13 +847,22 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
       }
       // release the stage (every read of it is above)
       __syncwarp();
-      if (leader && el_arrive_last(&empty[slot])) {
-        mbar_wait(&empty[slot], phase);
+      if (elect_one() && el_arrive_last_a(af + 8u * G::NS)) {
+        mbar_wait_a(af + 8u * G::NS, phase);
         if (pl + G::NS < nplanes) issue(pl + G::NS, slot);
+      }
+      if (CA) {
+        at_ = at_ + G::STAGE; ay = ay + G::STAGE; az = az + G::STAGE; afr = afr + G::STAGE;
+        af += 8u;
       }
       if (++slot == G::NS) {
         slot = 0;
         phase ^= 1u;
+        if (CA) {
+          at_ = at_ - G::NS * G::STAGE; ay = ay - G::NS * G::STAGE;
+          az = az - G::NS * G::STAGE; afr = afr - G::NS * G::STAGE;
+          af -= 8u * G::NS;
+        }
       }
       if (k >= 0) {
         constexpr int NO = PASS == 0 ? 3 : 6;
