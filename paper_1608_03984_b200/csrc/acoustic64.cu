@@ -251,7 +251,10 @@ struct QG64 {
 #ifdef FDR_A64_U
   static constexpr int U = FDR_A64_U;
 #else
-  static constexpr int U = R <= 2 ? QD : (R >= 7 ? 1 : 2);
+  // re-measured after the carried addresses (512^3 random levels, GPts/s):
+  // order 4 U = 1 205.2 vs whole-queue 201.0; orders 8 / 12 / 16 U = 3
+  // 169.0 / 141.8 / 124.8 vs U = 2 167.8 / 140.3 / 123.7 and U = 1 166.7 / 140.6 / 122.2
+  static constexpr int U = R <= 1 ? QD : (R == 2 ? 1 : 3);
 #endif
   static constexpr int NQ = 1 + LZ;  // double2 loads of the own z-row window
   static constexpr int NWARPS = QNT / 32;
