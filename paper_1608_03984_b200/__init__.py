@@ -6,6 +6,7 @@ Wavefield, dump_wavefield, max_stable_dt, oracle_step, run_benchmark, step) back
 sm_100a library libb200fd.so, plus the extensions the BASELINE configs need.
 """
 
+from ._inputs import invalidate_plan
 from .errors import DeviceError, ExtensionMissingError, FdroofError, ValidationError
 from .kernel import (
     BenchResult,

@@ -15,7 +15,7 @@ LIB_NAME = "libb200fd.so"
 LIB_PATH = os.environ.get("B200FD_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_RADIUS = 16
 
 FDR_OK, FDR_EINVAL, FDR_ECUDA = 0, -1, -2
@@ -110,7 +110,7 @@ EXPORTS = (
     ("fdr_acoustic_run", ctypes.c_int, (ctypes.POINTER(AcousticArgs), _vp)),
     ("fdr_acoustic_oracle_step", ctypes.c_int,
      (ctypes.POINTER(AcousticArgs), ctypes.POINTER(ctypes.c_double), ctypes.c_double,
-      ctypes.c_double, _vp)),
+      ctypes.c_double, _vp, _vp)),
     ("fdr_acoustic_workspace_bytes", ctypes.c_size_t, (ctypes.POINTER(AcousticArgs),)),
     (
         "fdr_acoustic_run_host",
@@ -131,6 +131,10 @@ EXPORTS = (
     ("fdr_acoustic_host_download", ctypes.c_int,
      (ctypes.POINTER(AcousticArgs), ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t, _vp)),
     ("fdr_last_launch_count", ctypes.c_int64, ()),
+    ("fdr_pending_error", ctypes.c_int, ()),
+    ("fdr_count_nonfinite", ctypes.c_int,
+     (_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+      ctypes.POINTER(ctypes.c_int64), _vp)),
     ("fdr_tti_args_size", ctypes.c_size_t, ()),
     ("fdr_tti_run", ctypes.c_int, (ctypes.c_void_p, _vp)),
     ("fdr_elastic_args_size", ctypes.c_size_t, ()),

@@ -104,6 +104,10 @@ def cmd_bench(args):
     print(f"of attainable:     {best.measured_gflops / point.attainable_gflops * 100.0:.1f}%")
     gpts = float(args.grid) ** 3 * args.nt / best.wall_time_s / 1e9
     print(f"updates:           {fmt(gpts)} GPts/s")
+    bad = best.wavefield.nonfinite_count()
+    print(f"final field:       {'finite' if bad == 0 else f'{bad} NaN/inf values'}")
+    if bad:  # the failure check: a diverged run is a computation error
+        raise FdroofError(f"the final wavefield has {bad} non-finite values (unstable dt?)")
     if args.dump:
         kernel.dump_wavefield(results[-1].wavefield, args.dump)
         print(f"wrote {args.dump}")

@@ -83,8 +83,8 @@ A64_DEV void gather(const A64Step& a) {
   if (a.gather_row < 0) return;
   const int nthr = blockDim.x * blockDim.y;
   const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  const int i = b * nthr + threadIdx.x + blockDim.x * threadIdx.y;
-  if (i < a.n_rec) {
+  const int stride = nthr * (int)(gridDim.x * gridDim.y * gridDim.z);
+  for (int i = b * nthr + threadIdx.x + blockDim.x * threadIdx.y; i < a.n_rec; i += stride) {
     const int* r = a.rec + 3 * i;
     a.traces[(size_t)a.gather_row * a.n_rec + i] =
         a.cur[(size_t)r[0] * a.pitch_x + (size_t)r[1] * a.pitch_y + r[2]];
@@ -617,17 +617,11 @@ static int stream_launch(const A64Step& s, cudaStream_t st, int* chunk_cache) {
   using G = Geo<R>;
   const bool sponge = s.gx != nullptr;
   auto kern = sponge ? a64_stream<R, true> : a64_stream<R, false>;
-  static int occ[2] = {0, 0}, nsm = 0, cfg_dev[2] = {-1, -1};
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  if (cfg_dev[sponge] != dev) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[sponge], kern, NT, 0);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return cuda_fail(e, "fp64 stream kernel occupancy");
-    if (occ[sponge] < 1) return fail(FDR_ECUDA, "fp64 stream kernel (r=%d) cannot be resident", R);
-    cfg_dev[sponge] = dev;
-  }
+  int occ_s = 0, nsm = 0;
+  const int frc = fdr::launch_facts(reinterpret_cast<const void*>(kern), NT, 0, &occ_s, &nsm);
+  if (frc != FDR_OK) return frc;
+  int occ[2] = {occ_s, occ_s};
+  cudaError_t e = cudaSuccess;
   const int tzn = (s.nz + TZ - 1) / TZ, tyn = (s.ny + TY - 1) / TY;
   if (*chunk_cache <= 0) {  // fewest waves x (planes + the 2r-plane queue fill)
     const long tiles = (long)tzn * tyn, slots = (long)occ[sponge] * nsm;
@@ -852,7 +846,8 @@ __global__ void div64_selftest_kernel(long long n, double m_lo, double m_hi, uns
 // into the scratch level; the on-grid source added to the new value in
 // float32 (kernel.py:167-173).  One thread per interior point.
 __global__ void __launch_bounds__(256) conv64_step(const float* cur, const float* prev, float* out,
-                                                   const float* m, double m_scalar, int nx, int ny,
+                                                   const float* m, const double* m64,
+                                                   double m_scalar, int nx, int ny,
                                                    int nz, int pitch_y, long long pitch_x, int r,
                                                    const double* __restrict__ w, double coef,
                                                    int sx, int sy, int sz, float q) {
@@ -875,7 +870,7 @@ __global__ void __launch_bounds__(256) conv64_step(const float* cur, const float
       acc = __dadd_rn(acc, __dmul_rn(w[j], at(x, y, z + o)));
     }
   }
-  const double mm = m ? (double)m[p] : m_scalar;
+  const double mm = m64 ? m64[p] : m ? (double)m[p] : m_scalar;
   const double upd = __dadd_rn(__dsub_rn(__dmul_rn(2.0, c), (double)prev[p]),
                                __ddiv_rn(__dmul_rn(coef, acc), mm));
   float v = __double2float_rn(upd);
@@ -909,7 +904,7 @@ int64_t fdr_selftest_division64(int64_t n, double m_lo, double m_hi, uint32_t se
 
 
 int fdr_acoustic_oracle_step(const fdr_acoustic_args* a, const double* weights64, double coef64,
-                             double m_scalar64, void* stream) {
+                             double m_scalar64, const double* m64, void* stream) {
   using fdr64::cuda_fail;
   using fdr64::fail;
   if (!a || a->abi_version != FDR_ABI_VERSION) return fail(FDR_EINVAL, "ABI version mismatch");
@@ -936,8 +931,8 @@ int fdr_acoustic_oracle_step(const fdr_acoustic_args* a, const double* weights64
   if (e == cudaSuccess) {
     dim3 grid((a->nz + 255) / 256, a->ny, a->nx);
     fdr64::conv64_step<<<grid, 256, 0, st>>>(
-        a->levels[2], a->levels[1], a->levels[0], a->m_mode == FDR_M_GRID ? a->m : nullptr,
-        a->m_mode == FDR_M_NONE ? 1.0 : m_scalar64, a->nx, a->ny, a->nz, a->pitch_y, a->pitch_x,
+        a->levels[2], a->levels[1], a->levels[0], a->m_mode == FDR_M_GRID ? a->m : nullptr, m64,
+        m_scalar64, a->nx, a->ny, a->nz, a->pitch_y, a->pitch_x,
         r, dw, coef64, inject ? a->src_x : -1, a->src_y, a->src_z, q);
     e = cudaGetLastError();
   }

@@ -76,8 +76,8 @@ __device__ void gather_vz(const ElStep& a) {
   const int nthr = blockDim.x * blockDim.y * blockDim.z;
   const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   const int t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-  const int i = b * nthr + t;
-  if (i < a.n_rec) {
+  const int stride = nthr * (int)(gridDim.x * gridDim.y * gridDim.z);
+  for (int i = b * nthr + t; i < a.n_rec; i += stride) {
     const int* q = a.rec + 3 * i;
     a.traces[(size_t)a.gather_row * a.n_rec + i] =
         a.f[VZ][(size_t)q[0] * a.pitch_x + (size_t)q[1] * a.pitch_y + q[2]];
@@ -904,15 +904,12 @@ static int elq_launch(const ElStep& s, const fdr_elastic_args* a, cudaStream_t s
   using G = QGeoE<R, PASS>;
   const bool sponge = s.gx != nullptr;
   auto kern = sponge ? el_queue<R, PASS, true> : el_queue<R, PASS, false>;
-  static int configured[2] = {-1, -1}, occ[2] = {1, 1};
+  int occ_s = 0, nsm_s = 0;
+  const int frc = fdr::launch_facts(reinterpret_cast<const void*>(kern), QN, G::SMEM, &occ_s, &nsm_s);
+  if (frc != FDR_OK) return frc;
+  int occ[2] = {occ_s, occ_s};
   int dev = 0;
   EL_CUDA(cudaGetDevice(&dev));
-  if (configured[sponge] != dev) {
-    EL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-    EL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[sponge], kern, QN, G::SMEM));
-    if (occ[sponge] < 1) return fail(FDR_ECUDA, "elastic queue kernel (r=%d) cannot be resident", R);
-    configured[sponge] = dev;
-  }
   const int tzn = (a->nz + QZ - 1) / QZ, tyn = (a->ny + QY - 1) / QY;
   if (*chunk_cache <= 0) {
     int nsm = 148;

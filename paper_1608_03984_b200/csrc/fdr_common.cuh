@@ -20,6 +20,13 @@ namespace fdr {
 int fail(int code, const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* what);
 
+// Resident CTAs per SM (*occ) and SM count (*nsm) of `kern` with `threads`
+// threads and `smem` dynamic shared bytes on the current device (also sets
+// the kernel's dynamic shared-memory limit).  Computed once per (kernel,
+// device, threads, smem) under a lock, so host threads driving several
+// devices never see another device's answer.  FDR_OK or an error code.
+int launch_facts(const void* kern, int threads, size_t smem, int* occ, int* nsm);
+
 // lap + w * (a + b): one tap pair of kernel.py:205 (three roundings).
 FDR_DEV float tap(float lap, float w, float a, float b) {
   return __fadd_rn(lap, __fmul_rn(w, __fadd_rn(a, b)));

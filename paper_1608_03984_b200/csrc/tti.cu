@@ -106,8 +106,8 @@ __device__ void gather(const TTIStep& a) {
   const int nthr = blockDim.x * blockDim.y * blockDim.z;
   const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   const int t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-  const int i = b * nthr + t;
-  if (i < a.n_rec) {
+  const int stride = nthr * (int)(gridDim.x * gridDim.y * gridDim.z);
+  for (int i = b * nthr + t; i < a.n_rec; i += stride) {
     const int* c = a.rec + 3 * i;
     a.traces[(size_t)a.gather_row * a.n_rec + i] =
         a.p[(size_t)c[0] * a.pitch_x + (size_t)c[1] * a.pitch_y + c[2]];
@@ -752,17 +752,9 @@ static int stream_inst(const TTIStep& s, const fdr_tti_args* a, int k, cudaStrea
   const bool sponge = s.gx != nullptr;
   auto kern = PACK ? (sponge ? tti_pack<R, true> : tti_pack<R, false>)
                    : (sponge ? tti_stream<R, true> : tti_stream<R, false>);
-  static int configured[2] = {-1, -1};
-  static int occ = 1, nsm = 148;
-  int dev = 0;
-  TTI_CUDA(cudaGetDevice(&dev));
-  if (configured[sponge] != dev) {
-    TTI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-    TTI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TNT, G::SMEM));
-    TTI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    if (occ < 1) return fail(FDR_ECUDA, "TTI stream kernel (r=%d) cannot be resident", R);
-    configured[sponge] = dev;
-  }
+  int occ = 0, nsm = 0;
+  const int frc = fdr::launch_facts(reinterpret_cast<const void*>(kern), TNT, G::SMEM, &occ, &nsm);
+  if (frc != FDR_OK) return frc;
   TTIMaps maps;
   const int cur = (2 + k) % 3, prev = (1 + k) % 3;
   int rc = tti_encode(&maps.box_p, a->p[cur], a, G::BZ, G::BY);

@@ -21,6 +21,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
+from ._inputs import InputGuard, cached_plan, config_inputs, host_tensor
 from .errors import ValidationError
 from .kernel import Receivers, Source, Sponge, StabilityWarning, row_pitch
 from .stencils import staggered_first_derivative_weights
@@ -152,12 +153,18 @@ class ElasticWavefield:
     def numpy(self, name: str) -> np.ndarray:
         return self.fields[FIELDS.index(name)][:, :, : self._dims[2]].cpu().numpy().copy()
 
+    def nonfinite_count(self, name: str = "vz") -> int:
+        """NaN/inf values of one field, counted on the device."""
+        from .kernel import count_nonfinite
+
+        return count_nonfinite(self.fields[FIELDS.index(name)], self._dims)
+
     def set_interior(self, name: str, values) -> None:
         torch = _torch()
         arr = np.ascontiguousarray(np.asarray(values, dtype=np.float32))
         if arr.shape != self._dims:
             raise ValidationError("interior values do not match dims")
-        self.fields[FIELDS.index(name)][:, :, : self._dims[2]].copy_(torch.from_numpy(arr))
+        self.fields[FIELDS.index(name)][:, :, : self._dims[2]].copy_(host_tensor(arr))
 
 
 class _ElArgs(ctypes.Structure):
@@ -181,30 +188,34 @@ class _ElArgs(ctypes.Structure):
 class _ElPlan:
     def __init__(self, cfg: ElasticConfig, device, pitch: int):
         torch = _torch()
-        self.key = _el_key(cfg, device)
+        self.key = _el_key(cfg, device, pitch)
+        self.guard = InputGuard(config_inputs(cfg, _EL_FIELDS))  # frozen while cached
         nx, ny, nz = cfg.dims
         self.c = elastic_weights_f32(cfg.order)
         self.params = []
         for host in cfg.params().values():
             t = torch.zeros((nx, ny, pitch), dtype=torch.float32, device=device)
-            t[:, :, :nz].copy_(torch.from_numpy(host))
+            t[:, :, :nz].copy_(host_tensor(host))
             self.params.append(t)
         self.sponge = None if cfg.sponge is None else tuple(
-            torch.from_numpy(v).to(device) for v in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
+            host_tensor(v).to(device) for v in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
         self.series, self.src, self.n_series = None, (-1, 0, 0), 0
         if cfg.source is not None:
             s = np.ascontiguousarray(np.asarray(cfg.source.series).astype(np.float32).reshape(-1))
-            self.series = torch.from_numpy(s).to(device)
+            self.series = host_tensor(s).to(device)
             self.src = tuple(int(v) for v in cfg.source.location)
             self.n_series = int(s.size)
         self.rec = None
         if cfg.receivers is not None:
-            self.rec = torch.from_numpy(cfg.receivers.locations.reshape(-1).copy()).to(device)
+            self.rec = host_tensor(cfg.receivers.locations.reshape(-1).copy()).to(device)
 
 
-def _el_key(cfg, device):
-    return (cfg.order, tuple(cfg.dims), float(cfg.dt), float(cfg.h), id(cfg.vp), id(cfg.vs),
-            id(cfg.rho), id(cfg.source), id(cfg.receivers), id(cfg.sponge), str(device))
+_EL_FIELDS = ("vp", "vs", "rho")
+
+
+def _el_key(cfg, device, pitch):
+    return (cfg.order, tuple(cfg.dims), float(cfg.dt), float(cfg.h),
+            tuple(id(o) for o in config_inputs(cfg, _EL_FIELDS)), str(device), int(pitch))
 
 
 _VARIANTS = {"auto": 0, "direct": 1, "stream": 2, "queue": 3}
@@ -228,10 +239,8 @@ def elastic_run(fld: ElasticWavefield, cfg: ElasticConfig, n_steps: Optional[int
     lib = _lib.load()
     dev = fld.device
     pitch_y = int(fld.fields[0].shape[2])
-    plan = getattr(cfg, "_device_plan", None)
-    if plan is None or plan.key != _el_key(cfg, dev):
-        plan = _ElPlan(cfg, dev, pitch_y)
-        cfg._device_plan = plan
+    plan = cached_plan(cfg, "_device_plan", _el_key(cfg, dev, pitch_y),
+                       lambda: _ElPlan(cfg, dev, pitch_y))
     a = _ElArgs()
     a.abi_version = _lib.ABI_VERSION
     a.order = cfg.order

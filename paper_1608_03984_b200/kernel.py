@@ -23,6 +23,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
+from ._inputs import InputGuard, cached_plan, config_inputs, host_tensor, invalidate_plan  # noqa: F401
 from .errors import ValidationError
 from .roofline import (
     ACOUSTIC_BYTES_PER_POINT,
@@ -284,7 +285,12 @@ class Wavefield:
         arr = np.ascontiguousarray(np.asarray(values, dtype=self._np_dtype))
         if arr.shape != self._dims:
             raise ValidationError(f"interior values of shape {arr.shape} do not match dims {self._dims}")
-        self.interior(level).copy_(torch.from_numpy(arr))
+        self.interior(level).copy_(host_tensor(arr))
+
+    def nonfinite_count(self, level: int = 2) -> int:
+        """NaN/inf values in a level, counted on the device (the end-of-run
+        failure check; fdr_count_nonfinite)."""
+        return count_nonfinite(self.grids[level], self._dims)
 
     def halo_is_zero(self) -> bool:
         """The halo is not stored; row-padding columns must stay zero."""
@@ -317,6 +323,23 @@ class Wavefield:
         return fld
 
 
+def count_nonfinite(t, dims) -> int:
+    """Number of NaN/inf interior values of one (nx, ny, pitch) device level."""
+    torch = _torch()
+    if not t.is_cuda or t.dtype not in (torch.float32, torch.float64) or not t.is_contiguous():
+        raise ValidationError("count_nonfinite takes a contiguous float32/float64 CUDA level")
+    lib = _lib.load()
+    n = ctypes.c_int64(0)
+    pitch_y = int(t.shape[2])
+    with torch.cuda.device(t.device):
+        stream = torch.cuda.current_stream(t.device).cuda_stream
+        _lib.check(lib.fdr_count_nonfinite(ctypes.c_void_p(t.data_ptr()), t.element_size(),
+                                           *(int(d) for d in dims), pitch_y,
+                                           int(t.shape[1]) * pitch_y, ctypes.byref(n),
+                                           ctypes.c_void_p(stream)))
+    return int(n.value)
+
+
 def _check_match(fld: Wavefield, cfg: KernelConfig):
     if fld.halo != cfg.halo or fld.dims != tuple(cfg.dims):
         raise ValidationError(
@@ -331,7 +354,7 @@ class _DevicePlan:
     def __init__(self, cfg: KernelConfig, device, pitch: int):
         torch = _torch()
         self.key = _plan_key(cfg, device)
-        self.refs = (cfg.m, cfg.source, cfg.receivers, cfg.sponge)  # keep ids alive
+        self.guard = InputGuard(config_inputs(cfg, ("m",)))  # frozen while cached
         nx, ny, nz = cfg.dims
         self.weights = acoustic_weights_f32(cfg.order)
         self.coef = np.float32(cfg.dt * cfg.dt / (cfg.h * cfg.h))  # kernel.py:187
@@ -346,22 +369,22 @@ class _DevicePlan:
             host = np.asarray(cfg.m, dtype=np.float32)  # kernel.py:188
             self.m_bounds = (float(host.min()), float(host.max()))
             self.m_grid = torch.zeros((nx, ny, pitch), dtype=torch.float32, device=device)
-            self.m_grid[:, :, :nz].copy_(torch.from_numpy(np.ascontiguousarray(host)))
+            self.m_grid[:, :, :nz].copy_(host_tensor(np.ascontiguousarray(host)))
         self.sponge = None
         if cfg.sponge is not None:
             self.sponge = tuple(
-                torch.from_numpy(p).to(device) for p in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z)
+                host_tensor(p).to(device) for p in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z)
             )
         self.series = None
         self.src = (-1, 0, 0)
         self.src_w = None
         if cfg.source is not None:
             series = np.asarray(cfg.source.series).astype(np.float32)  # kernel.py:173
-            self.series = torch.from_numpy(np.ascontiguousarray(series.reshape(-1))).to(device)
+            self.series = host_tensor(np.ascontiguousarray(series.reshape(-1))).to(device)
             if isinstance(cfg.source, OffGridSource):
                 base, w = trilinear_weights([cfg.source.position])
                 self.src = tuple(int(c) for c in base[0])
-                self.src_w = torch.from_numpy(np.ascontiguousarray(w[0])).to(device)
+                self.src_w = host_tensor(np.ascontiguousarray(w[0])).to(device)
             else:
                 self.src = tuple(int(c) for c in cfg.source.location)
         self.n_series = 0 if self.series is None else int(self.series.numel())
@@ -369,23 +392,22 @@ class _DevicePlan:
         self.rec_w = None
         if isinstance(cfg.receivers, OffGridReceivers):
             base, w = trilinear_weights(cfg.receivers.positions)
-            self.rec = torch.from_numpy(base.reshape(-1).copy()).to(device)
-            self.rec_w = torch.from_numpy(np.ascontiguousarray(w.reshape(-1))).to(device)
+            self.rec = host_tensor(base.reshape(-1).copy()).to(device)
+            self.rec_w = host_tensor(np.ascontiguousarray(w.reshape(-1))).to(device)
         elif cfg.receivers is not None:
-            self.rec = torch.from_numpy(cfg.receivers.locations.reshape(-1).copy()).to(device)
+            self.rec = host_tensor(cfg.receivers.locations.reshape(-1).copy()).to(device)
 
 
-def _plan_key(cfg: KernelConfig, device):
-    return (cfg.order, tuple(cfg.dims), float(cfg.dt), float(cfg.h), id(cfg.m),
-            id(cfg.source), id(cfg.receivers), id(cfg.sponge), str(device))
+def _plan_key(cfg: KernelConfig, device, pitch: int = 0):
+    """Plan identity: the scalars plus the identities of the input arrays
+    (which the plan holds and write-protects, see _inputs.py)."""
+    return (cfg.order, tuple(cfg.dims), float(cfg.dt), float(cfg.h),
+            tuple(id(o) for o in config_inputs(cfg, ("m",))), str(device), int(pitch))
 
 
 def _plan(cfg: KernelConfig, device, pitch: int) -> _DevicePlan:
-    plan = getattr(cfg, "_device_plan", None)
-    if plan is None or plan.key != _plan_key(cfg, device):
-        plan = _DevicePlan(cfg, device, pitch)
-        cfg._device_plan = plan
-    return plan
+    return cached_plan(cfg, "_device_plan", _plan_key(cfg, device, pitch),
+                       lambda: _DevicePlan(cfg, device, pitch))
 
 
 def _ptr(t) -> Optional[int]:
@@ -447,9 +469,6 @@ def run(fld: Wavefield, cfg: KernelConfig, n_steps: Optional[int] = None,
     pitch_y = int(fld.grids[0].shape[2])
     pitch_x = int(fld.grids[0].shape[1]) * pitch_y
     plan = _plan(cfg, dev, pitch_y)
-    if plan.m_grid is not None and tuple(plan.m_grid.shape) != tuple(fld.grids[0].shape):
-        plan = _DevicePlan(cfg, dev, pitch_y)
-        cfg._device_plan = plan
     args = _lib.AcousticArgs()
     _fill_args(args, cfg, plan, fld.dims, pitch_y, pitch_x, fld.it, n, _VARIANTS[variant])
     args.m = _ptr(plan.m_grid)
@@ -487,8 +506,8 @@ class _DevicePlan64:
 
     def __init__(self, cfg: KernelConfig, device, pitch: int):
         torch = _torch()
-        self.key = _plan_key(cfg, device)
-        self.refs = (cfg.m, cfg.source, cfg.receivers, cfg.sponge)
+        self.key = _plan_key(cfg, device, pitch)
+        self.guard = InputGuard(config_inputs(cfg, ("m",)))
         nx, ny, nz = cfg.dims
         r = cfg.order // 2
         w = [float(x) for x in second_derivative_weights(cfg.order)]
@@ -503,21 +522,21 @@ class _DevicePlan64:
             self.m_mode = _lib.M_GRID
             host = np.ascontiguousarray(np.asarray(cfg.m, dtype=np.float64))
             self.m_grid = torch.zeros((nx, ny, pitch), dtype=torch.float64, device=device)
-            self.m_grid[:, :, :nz].copy_(torch.from_numpy(host))
+            self.m_grid[:, :, :nz].copy_(host_tensor(host))
         self.sponge = None
         if cfg.sponge is not None:
-            self.sponge = tuple(torch.from_numpy(np.asarray(p, dtype=np.float64)).to(device)
+            self.sponge = tuple(host_tensor(np.asarray(p, dtype=np.float64)).to(device)
                                 for p in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
         self.series = None
         self.src = (-1, 0, 0)
         if cfg.source is not None:
             series = np.ascontiguousarray(np.asarray(cfg.source.series, dtype=np.float64).reshape(-1))
-            self.series = torch.from_numpy(series).to(device)
+            self.series = host_tensor(series).to(device)
             self.src = tuple(int(c) for c in cfg.source.location)
         self.n_series = 0 if self.series is None else int(self.series.numel())
         self.rec = None
         if cfg.receivers is not None:
-            self.rec = torch.from_numpy(cfg.receivers.locations.reshape(-1).copy()).to(device)
+            self.rec = host_tensor(cfg.receivers.locations.reshape(-1).copy()).to(device)
 
 
 def _run_f64(fld: Wavefield, cfg: KernelConfig, n: int, variant: str) -> Wavefield:
@@ -531,11 +550,8 @@ def _run_f64(fld: Wavefield, cfg: KernelConfig, n: int, variant: str) -> Wavefie
         raise ValidationError("the float64 path takes on-grid sources and receivers")
     pitch_y = int(fld.grids[0].shape[2])
     pitch_x = int(fld.grids[0].shape[1]) * pitch_y
-    plan = getattr(cfg, "_device_plan64", None)
-    if (plan is None or plan.key != _plan_key(cfg, dev)
-            or (plan.m_grid is not None and tuple(plan.m_grid.shape) != tuple(fld.grids[0].shape))):
-        plan = _DevicePlan64(cfg, dev, pitch_y)
-        cfg._device_plan64 = plan
+    plan = cached_plan(cfg, "_device_plan64", _plan_key(cfg, dev, pitch_y),
+                       lambda: _DevicePlan64(cfg, dev, pitch_y))
     a = _lib.Acoustic64Args()
     a.abi_version = _lib.ABI_VERSION
     a.order = cfg.order
@@ -635,9 +651,6 @@ def oracle_step(fld: Wavefield, cfg: KernelConfig) -> Wavefield:
     pitch_y = int(fld.grids[0].shape[2])
     pitch_x = int(fld.grids[0].shape[1]) * pitch_y
     plan = _plan(cfg, dev, pitch_y)
-    if plan.m_grid is not None and tuple(plan.m_grid.shape) != tuple(fld.grids[0].shape):
-        plan = _DevicePlan(cfg, dev, pitch_y)
-        cfg._device_plan = plan
     args = _lib.AcousticArgs()
     _fill_args(args, cfg, plan, fld.dims, pitch_y, pitch_x, fld.it, 1, _lib.VARIANT_AUTO)
     args.m = _ptr(plan.m_grid)
@@ -648,11 +661,18 @@ def oracle_step(fld: Wavefield, cfg: KernelConfig) -> Wavefield:
     w = second_derivative_weights(cfg.order)  # exact rationals, as fd_weights
     w64 = (ctypes.c_double * (r + 1))(float(3 * w[r]), *(float(w[r + j]) for j in range(1, r + 1)))
     coef = float(cfg.dt) ** 2 / float(cfg.h) ** 2  # kernel.py:246
+    # the reference divides by cfg.m itself (kernel.py:247): a scalar even when
+    # it is 1, a grid as float64 (a float64 grid must not be rounded to float32)
     m_scalar = float(cfg.m) if np.isscalar(cfg.m) else 1.0
+    m64 = None
+    if not np.isscalar(cfg.m) and np.asarray(cfg.m).dtype != np.float32:
+        host = np.ascontiguousarray(np.asarray(cfg.m, dtype=np.float64))
+        m64 = torch.zeros(tuple(fld.grids[0].shape), dtype=torch.float64, device=dev)
+        m64[:, :, : fld.dims[2]].copy_(host_tensor(host))
     stream = torch.cuda.current_stream(dev).cuda_stream
     with torch.cuda.device(dev):
         _lib.check(lib.fdr_acoustic_oracle_step(ctypes.byref(args), w64, coef, m_scalar,
-                                                ctypes.c_void_p(stream)))
+                                                _ptr(m64), ctypes.c_void_p(stream)))
     scratch, prev, cur = fld.grids
     fld.grids = [prev, cur, scratch]
     fld.it += 1
@@ -791,7 +811,7 @@ class HostSimulation:
         def pinned(arr):
             if arr is None:
                 return None
-            t = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+            t = host_tensor(np.ascontiguousarray(arr)).pin_memory()
             return t
 
         self.h_m = pinned(plan.m_host)

@@ -27,6 +27,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
+from ._inputs import InputGuard, cached_plan, config_inputs, host_tensor
 from .errors import ValidationError
 from .kernel import Receivers, Source, Sponge, StabilityWarning, row_pitch
 from .stencils import first_derivative_weights, second_derivative_weights
@@ -179,12 +180,18 @@ class TTIWavefield:
         t = (self.p if field == "p" else self.r)[level]
         return t[:, :, : self._dims[2]].cpu().numpy().copy()
 
+    def nonfinite_count(self, field: str = "p", level: int = 2) -> int:
+        """NaN/inf values of a field's level, counted on the device."""
+        from .kernel import count_nonfinite
+
+        return count_nonfinite((self.p if field == "p" else self.r)[level], self._dims)
+
     def set_interior(self, field: str, level: int, values) -> None:
         torch = _torch()
         arr = np.ascontiguousarray(np.asarray(values, dtype=np.float32))
         if arr.shape != self._dims:
             raise ValidationError("interior values do not match dims")
-        (self.p if field == "p" else self.r)[level][:, :, : self._dims[2]].copy_(torch.from_numpy(arr))
+        (self.p if field == "p" else self.r)[level][:, :, : self._dims[2]].copy_(host_tensor(arr))
 
 
 class _TTIArgs(ctypes.Structure):
@@ -208,31 +215,34 @@ class _TTIArgs(ctypes.Structure):
 class _TTIPlan:
     def __init__(self, cfg: TTIConfig, device, pitch: int):
         torch = _torch()
-        self.key = _tti_key(cfg, device)
+        self.key = _tti_key(cfg, device, pitch)
+        self.guard = InputGuard(config_inputs(cfg, _TTI_FIELDS))  # frozen while cached
         nx, ny, nz = cfg.dims
         self.w2, self.w1 = tti_weights_f32(cfg.order)
         self.params = []
         for name, host in cfg.params().items():
             t = torch.zeros((nx, ny, pitch), dtype=torch.float32, device=device)
-            t[:, :, :nz].copy_(torch.from_numpy(host))
+            t[:, :, :nz].copy_(host_tensor(host))
             self.params.append(t)
         self.sponge = None if cfg.sponge is None else tuple(
-            torch.from_numpy(v).to(device) for v in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
+            host_tensor(v).to(device) for v in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
         self.series, self.src, self.n_series = None, (-1, 0, 0), 0
         if cfg.source is not None:
             s = np.ascontiguousarray(np.asarray(cfg.source.series).astype(np.float32).reshape(-1))
-            self.series = torch.from_numpy(s).to(device)
+            self.series = host_tensor(s).to(device)
             self.src = tuple(int(c) for c in cfg.source.location)
             self.n_series = int(s.size)
         self.rec = None
         if cfg.receivers is not None:
-            self.rec = torch.from_numpy(cfg.receivers.locations.reshape(-1).copy()).to(device)
+            self.rec = host_tensor(cfg.receivers.locations.reshape(-1).copy()).to(device)
 
 
-def _tti_key(cfg, device):
-    return (cfg.order, tuple(cfg.dims), float(cfg.dt), float(cfg.h), id(cfg.m), id(cfg.epsilon),
-            id(cfg.delta), id(cfg.theta), id(cfg.phi), id(cfg.source), id(cfg.receivers),
-            id(cfg.sponge), str(device))
+_TTI_FIELDS = ("m", "epsilon", "delta", "theta", "phi")
+
+
+def _tti_key(cfg, device, pitch):
+    return (cfg.order, tuple(cfg.dims), float(cfg.dt), float(cfg.h),
+            tuple(id(o) for o in config_inputs(cfg, _TTI_FIELDS)), str(device), int(pitch))
 
 
 _VARIANTS = {"auto": 0, "direct": 1, "stream": 2, "queue": 3}
@@ -256,10 +266,8 @@ def tti_run(fld: TTIWavefield, cfg: TTIConfig, n_steps: Optional[int] = None,
     lib = _lib.load()
     dev = fld.device
     pitch_y = int(fld.p[0].shape[2])
-    plan = getattr(cfg, "_device_plan", None)
-    if plan is None or plan.key != _tti_key(cfg, dev):
-        plan = _TTIPlan(cfg, dev, pitch_y)
-        cfg._device_plan = plan
+    plan = cached_plan(cfg, "_device_plan", _tti_key(cfg, dev, pitch_y),
+                       lambda: _TTIPlan(cfg, dev, pitch_y))
     a = _TTIArgs()
     a.abi_version = _lib.ABI_VERSION
     a.order = cfg.order

@@ -1,0 +1,99 @@
+"""Receiver gathers with more receivers than a launch has threads.
+
+The in-kernel gathers (the first threads of each step's launch record the
+previous step's row) are grid-stride loops: a receiver at every interior
+point must be recorded by every kernel variant, bit-exact against the C
+oracles.  Reference semantics for the on-grid sample: the newest level at
+rec_i after injection (SURVEY.md §8(a') receivers; kernel.py:167-173 order).
+"""
+
+import numpy as np
+import pytest
+
+from cases import random_levels, sha
+
+pytestmark = pytest.mark.gpu
+
+ACOUSTIC_VARIANTS = ["queue", "tma", "direct", "persistent", "cluster"]
+
+
+@pytest.fixture(scope="module")
+def B(cuda_device):
+    import paper_1608_03984_b200 as pkg
+    from paper_1608_03984_b200 import _lib
+
+    _lib.load()
+    return pkg
+
+
+def every_point(dims):
+    g = np.stack(np.meshgrid(*(np.arange(d) for d in dims), indexing="ij"), -1)
+    return g.reshape(-1, 3)
+
+
+@pytest.mark.parametrize("variant", ACOUSTIC_VARIANTS)
+def test_acoustic_receiver_at_every_point(B, variant):
+    """40x64x64 = 163,840 receivers: more than the queue grid's threads and
+    than the persistent kernel's 148 x 1024."""
+    from oracle import acoustic as O
+    from oracle import cref
+
+    dims, order, n = (40, 64, 64), 4, 3
+    dt = 0.5 * B.max_stable_dt(order, 1.0)
+    series = np.array([1.0, -0.5, 0.25], np.float32)
+    cfg = B.KernelConfig(order=order, dims=dims, n_t=n, dt=dt,
+                         source=B.Source((20, 31, 33), series),
+                         receivers=B.Receivers(every_point(dims)))
+    cur, prev = random_levels(dims, 41)
+    fld = B.Wavefield.allocate(dims, cfg.halo)
+    fld.set_interior(2, cur)
+    fld.set_interior(1, prev)
+    try:
+        B.run(fld, cfg, n, variant=variant)
+    except B.ValidationError as e:
+        if variant == "cluster" and "cluster" in str(e):
+            pytest.skip(str(e))
+        raise
+    st = O.OracleState(dims, cfg.halo)
+    O.interior(st.grids[2], st.halo)[...] = cur
+    O.interior(st.grids[1], st.halo)[...] = prev
+    cref.simulate(cfg, n, state=st)
+    assert sha(fld.numpy()) == sha(st.latest())
+    got = fld.traces.cpu().numpy()
+    assert got.shape[1] == 163840
+    assert (got[:n] == st.traces[:n]).all()
+
+
+@pytest.mark.parametrize("variant", ["auto", "direct"])
+def test_tti_receiver_at_every_point(B, variant):
+    from oracle import tti as T
+    from paper_1608_03984_b200 import tti
+
+    dims, n = (24, 64, 64), 3
+    rec = B.Receivers(every_point(dims))
+    cfg = tti.TTIConfig(order=8, dims=dims, n_t=n, dt=1e-3, h=10.0, m=1.0 / 3000.0 ** 2,
+                        epsilon=0.2, delta=0.1, theta=0.4, phi=0.3,
+                        source=B.Source((12, 31, 30), np.array([1e3, -5e2, 2e2])), receivers=rec)
+    f = tti.TTIWavefield.allocate(dims, cfg.halo)
+    tti.tti_run(f, cfg, variant=variant)
+    w2, w1 = tti.tti_weights_f32(8)
+    st = T.simulate_c(cfg, cfg.params(), w2, w1)
+    assert sha(f.numpy("p")) == sha(st.interior("p"))
+    assert (f.traces.cpu().numpy()[:n] == st.traces[:n]).all()
+
+
+@pytest.mark.parametrize("variant", ["auto", "direct"])
+def test_elastic_receiver_at_every_point(B, variant):
+    from oracle import elastic as E
+    from paper_1608_03984_b200 import elastic
+
+    dims, n = (24, 64, 64), 3
+    rec = B.Receivers(every_point(dims))
+    cfg = elastic.ElasticConfig(order=8, dims=dims, n_t=n, dt=8e-4, h=10.0, vp=3000.0,
+                                vs=3000.0 / 1.8, rho=2000.0, receivers=rec,
+                                source=B.Source((12, 31, 30), np.array([1e6, -5e5, 2e5])))
+    f = elastic.ElasticWavefield.allocate(dims, cfg.halo)
+    elastic.elastic_run(f, cfg, variant=variant)
+    st = E.simulate_c(cfg, cfg.params(), elastic.elastic_weights_f32(8))
+    assert sha(f.numpy("vz")) == sha(st.interior("vz"))
+    assert (f.traces.cpu().numpy()[:n] == st.traces[:n]).all()
