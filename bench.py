@@ -12,9 +12,13 @@ traces inside the timed region; two simulations are in flight, so one's
 copies overlap the other's time steps (back-to-back shots).  Inputs (2.1 GB of
 levels + m) exceed the 126 MB L2, so no flush is needed between steps.
 
---impl reference times the reference's CPU algorithm (the oracle port of
-fdroof.kernel.step, numpy ufuncs with x-slab threads = host cores) on the
-same config: one bench step = one time step of the 512^3 grid.
+--impl reference times the reference's own CPU implementation on the same
+config: the unmodified fdroof.kernel.step (installed from /root/reference into
+baseline/_ref, which travels to the GPU box; numpy ufuncs with x-slab threads
+= host cores), driven like the reference's run loop (kernel.py:281-284) with
+the sponge taper, injection and receivers applied around it (SURVEY.md
+§8(a')).  One bench step = one time step of the 512^3 grid.  Without
+baseline/_ref the numpy port in oracle/ stands in (kind "port").
 
 Multi-GPU: replicas only: every rank runs its own independent
 simulation; the timed region is bracketed by barriers, the time is the max
@@ -53,7 +57,7 @@ def parse():
     p.add_argument("--no-sweep", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--cpu-steps", type=int, default=5)
     p.add_argument("--no-fp64", action="store_true", help="skip the float64 leg")
     p.add_argument("--no-configs", action="store_true",
                    help="skip the BASELINE configs 1, 3, 4, 5 lines")
@@ -148,38 +152,88 @@ def dist_setup(args):
     return world, rank, local
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_stepper(cfg, cores):
+    """One time step of the reference on the CPU, as a closure, and its kind.
+
+    "reference": the unmodified fdroof.kernel.step (baseline/_ref) on a
+    source-free copy of the config, then the sponge taper on the new level,
+    the injection of series[it] and the receiver sample -- the order of
+    SURVEY.md §8(a') (tests/golden/make_golden.py::run_extended).
+    "port": the numpy restatement oracle/acoustic.py::step (same result bit
+    for bit, tests/test_oracle.py), when baseline/_ref is absent."""
+    if os.path.isdir(os.path.join(REF_DIR, "fdroof")):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from fdroof import kernel as K
+
+        kcfg = K.KernelConfig(order=cfg.order, dims=tuple(cfg.dims), n_t=cfg.n_t, dt=cfg.dt,
+                              h=cfg.h, m=np.asarray(cfg.m, np.float32))
+        fld = K.Wavefield.allocate(kcfg.dims, kcfg.halo)
+        from oracle import acoustic as O
+
+        taper = O.sponge_taper(cfg)
+        r = kcfg.halo
+        series = np.asarray(cfg.source.series).astype(np.float32)
+        loc = tuple(c + r for c in cfg.source.location)
+        rec = cfg.receivers.locations
+        traces = np.zeros((cfg.n_t, rec.shape[0]), np.float32)
+
+        def one():
+            it = fld.it
+            K.step(fld, kcfg, slabs=cores)
+            new = fld.interior(2)
+            new *= taper
+            if it < len(series):
+                fld.grids[2][loc] += series[it]
+            traces[it % cfg.n_t] = new[rec[:, 0], rec[:, 1], rec[:, 2]]
+
+        one.latest = lambda: fld.interior(2)
+        return one, "reference", "unmodified fdroof.kernel.step (baseline/_ref)"
+    from oracle import acoustic as O
+
+    st = O.OracleState(cfg.dims, cfg.halo)
+    taper = O.sponge_taper(cfg)
+    st.traces = np.zeros((cfg.n_t, cfg.receivers.count), np.float32)
+
+    def one():
+        O.step(st, cfg, slabs=cores, taper=taper)
+
+    one.latest = st.latest
+    return one, "port", "numpy port of fdroof.kernel.step (oracle/acoustic.py)"
+
+
 def reference_arm(args):
-    """CPU reference algorithm (oracle port of fdroof.kernel.step) on rank 0."""
+    """The reference's CPU path (reference_stepper) on rank 0."""
     world, rank, _ = dist_setup(args)
     if rank != 0:
         return 0
-    from oracle import acoustic as O
     from paper_1608_03984_b200.synthetic import config2
 
     cores = len(os.sched_getaffinity(0))
     dims = (args.grid,) * 3
     cfg = config2(order=args.order, n_t=args.nt, dims=dims)
-    st = O.OracleState(cfg.dims, cfg.halo)
-    taper = O.sponge_taper(cfg)
-    st.traces = np.zeros((cfg.n_t, cfg.receivers.count), np.float32)
+    one, kind, what = reference_stepper(cfg, cores)
     for _ in range(args.warmup):
-        O.step(st, cfg, slabs=cores, taper=taper)
+        one()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        O.step(st, cfg, slabs=cores, taper=taper)
+        one()
     wall = time.perf_counter() - t0
     pts = float(np.prod(dims))
     value = pts * args.steps / wall / 1e9
     sample = (f"{args.steps} timed time-steps (after {args.warmup} warm-up) of the "
-              f"{dims[0]}^3 order-{args.order} update, numpy port of fdroof.kernel.step, "
-              f"slabs={cores}")
+              f"{dims[0]}^3 order-{args.order} update with sponge, source and receivers: "
+              f"{what}, slabs={cores}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded smooth random model, BASELINE config 2)",
         "config": workload_config(args),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -196,20 +250,20 @@ def workload_config(args):
 
 
 def cpu_baseline(args, cfg):
-    from oracle import acoustic as O
-
+    """The reference's CPU path on a bounded sample: args.cpu_steps time steps
+    (after one warm-up) of the same 512^3 workload."""
     cores = len(os.sched_getaffinity(0))
-    st = O.OracleState(cfg.dims, cfg.halo)
-    taper = O.sponge_taper(cfg)
-    O.step(st, cfg, slabs=cores, taper=taper)  # warm
+    one, kind, what = reference_stepper(cfg, cores)
+    one()  # warm
     t0 = time.perf_counter()
     for _ in range(args.cpu_steps):
-        O.step(st, cfg, slabs=cores, taper=taper)
+        one()
     wall = time.perf_counter() - t0
     value = float(np.prod(cfg.dims)) * args.cpu_steps / wall / 1e9
-    return {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{args.cpu_steps} time steps of the {cfg.dims[0]}^3 order-{cfg.order} "
-                      "update (numpy port of fdroof.kernel.step, x-slab threads)"}
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{args.cpu_steps} time steps (after 1 warm-up) of the {cfg.dims[0]}^3 "
+                      f"order-{cfg.order} update with sponge, source and receivers: {what}, "
+                      "x-slab threads = host cores"}
 
 
 def time_device(fn, reps=1):
@@ -229,6 +283,32 @@ def time_device(fn, reps=1):
     return a.elapsed_time(b) / reps
 
 
+def ncu_flops(key):
+    """ncu-counted FLOPs / DRAM bytes per point of a production kernel
+    (profiles/r02_ncu_flops.json, tools/ncu_flops.sh)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_flops.json"), encoding="utf-8") as fh:
+            return json.load(fh).get(key, {})
+    except (OSError, ValueError):
+        return {}
+
+
+def fp32_peak_tflops():
+    """The FP32 roofline denominator measured here and now (fdr_fp32_fma_peak:
+    FMA chains, no memory traffic), best of 3."""
+    import ctypes
+
+    from paper_1608_03984_b200 import _lib
+
+    lib = _lib.load()
+    best = 0.0
+    for _ in range(3):
+        tf = ctypes.c_double(0.0)
+        _lib.check(lib.fdr_fp32_fma_peak(20000, 1, ctypes.byref(tf), None))
+        best = max(best, tf.value)
+    return best
+
+
 def other_configs(dev, hbm):
     """BASELINE configs 1, 3, 4, 5, each run for its full n_t from zero fields
     (the acoustic ones with zeroed levels inside the timing)."""
@@ -237,7 +317,7 @@ def other_configs(dev, hbm):
     from paper_1608_03984_b200.synthetic import config1, config3
 
     out = {}
-    fp32_peak = RL.b200_machine().peak_gflops_achievable
+    fp32_peak = fp32_peak_tflops() * 1e3  # GFLOP/s, measured
     for name, cfg in (("config1", config1()), ("config3", config3())):
         fld = B.Wavefield.allocate(cfg.dims, cfg.halo, device=dev)
 
@@ -266,10 +346,19 @@ def other_configs(dev, hbm):
     ms = time_device(sim4)
     g = float(np.prod(cfg.dims)) * cfg.n_t / (ms / 1e3) / 1e9
     fl = tti.tti_flops_per_point(cfg.order)
-    out["config4"] = {"workload": f"TTI order 8, {cfg.dims}, {cfg.n_t} steps", "gpts_per_s": round(g, 2),
-                      "ms_per_sim": round(ms, 3), "gflops_catalog": round(g * fl, 1),
-                      "frac_fp32": round(g * fl / fp32_peak, 4), "bound": "fp32 (catalog OI 16.1)",
-                      "frac_hbm_60B": round(g * 60 / hbm, 4)}
+    counted = ncu_flops("tti_config4_384^3").get("void tti_pack<4, 1>", {})
+    fl_ncu = counted.get("flops_per_point")
+    out["config4"] = {
+        "workload": f"TTI order 8, {cfg.dims}, {cfg.n_t} steps", "gpts_per_s": round(g, 2),
+        "ms_per_sim": round(ms, 3),
+        # the bound is set by the FLOPs the kernel executes (ncu), not the
+        # catalogue's 964/pt: 242/pt over 60 B/pt is OI 4.0, below the ridge
+        "bound": "hbm (60 B/pt; measured OI below the FP32 ridge)",
+        "frac_hbm_60B": round(g * 60 / hbm, 4),
+        "flops_per_point_ncu": fl_ncu, "dram_bytes_per_point_ncu": counted.get("dram_bytes_per_point"),
+        "fp32_peak_gflops_measured": round(fp32_peak, 1),
+        "frac_fp32_ncu_flops": round(g * fl_ncu / fp32_peak, 4) if fl_ncu else None,
+        "gflops_catalog": round(g * fl, 1), "flops_per_point_catalog": fl}
     del fld
     cfg = elastic.config5()
     fld = elastic.ElasticWavefield.allocate(cfg.dims, cfg.halo, device=dev)
@@ -282,10 +371,13 @@ def other_configs(dev, hbm):
 
     ms = time_device(sim5)
     g = float(np.prod(cfg.dims)) * cfg.n_t / (ms / 1e3) / 1e9
+    el = ncu_flops("elastic_config5_320^3")
+    moved = sum(v.get("dram_bytes_per_point", 0.0) for v in el.values()) or None
     out["config5"] = {"workload": f"elastic velocity-stress order 8, {cfg.dims}, {cfg.n_t} steps",
                       "gpts_per_s": round(g, 2), "ms_per_sim": round(ms, 3),
                       "frac_hbm_84B": round(g * 84 / hbm, 4), "bound": "hbm (84 B/pt)",
-                      "two_pass_gbs_120B": round(g * 120, 1)}
+                      "dram_bytes_per_point_ncu": moved,
+                      "frac_hbm_moved": round(g * moved / hbm, 4) if moved else None}
     return out
 
 
@@ -313,6 +405,49 @@ def fp64_leg(dev, cfg, hbm, final32):
             "gpts_per_s": round(g, 2), "ms_per_sim": round(ms, 3), "bytes_per_point": 32,
             "frac_hbm": round(g * 32 / hbm, 4), "kernel": f"a64_queue<R={cfg.order // 2}> (AUTO)",
             "f32_rel_l2_vs_f64": err}
+
+
+def step_loop_leg(cfg, dev, npts):
+    """The reference's own calling pattern through the public API: one
+    `step(fld, cfg)` call per time step (kernel.py:281-284).  Each timed shot
+    uploads the config's inputs again (invalidate_plan, then the first step
+    builds the device plan: m, sponge, series, receivers), zeroes the levels,
+    makes n_t step() calls and downloads the final level and the traces;
+    CUDA events bracket all of it on the compute stream."""
+    import torch
+
+    import paper_1608_03984_b200 as B
+
+    fld = B.Wavefield.allocate(cfg.dims, cfg.halo, device=dev)
+    out = {}
+
+    def shot():
+        B.invalidate_plan(cfg)
+        for g in fld.grids:
+            g.zero_()
+        fld.it = 0
+        for _ in range(cfg.n_t):
+            B.step(fld, cfg)
+        out["final"] = fld.numpy(2)
+        out["traces"] = fld.traces.cpu().numpy()
+
+    shot()
+    torch.cuda.synchronize(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    shot()
+    b.record()
+    b.synchronize()
+    ms = a.elapsed_time(b)
+    h2d = int(np.asarray(cfg.m, np.float32).nbytes + 4 * sum(len(p) for p in
+                                                             (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
+              + 4 * len(cfg.source.series) + 12 * cfg.receivers.count)
+    d2h = int(out["final"].nbytes + out["traces"].nbytes)
+    del fld
+    return {"value": round(npts * cfg.n_t / (ms / 1e3) / 1e9, 3), "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_sim": round(ms, 3),
+            "api": "invalidate_plan(cfg); n_t x step(fld, cfg); fld.numpy(); fld.traces.cpu() "
+                   "(the reference's per-step loop, kernel.py:281-284)"}
 
 
 def load_ncu_traffic(order):
@@ -410,6 +545,7 @@ def main():
                       "_download (each shot uploads its inputs and downloads its final level "
                       "and traces; steps on one stream, copies on two)"}
         del sim
+        e2e["step_loop"] = step_loop_leg(cfg, dev, npts)
 
     # per-order sweep (config 2 is a sweep over orders 2..16)
     sweep = []

@@ -62,7 +62,7 @@ class InputGuard:
             if isinstance(o, np.ndarray):
                 if not any(o is a for a in arrays):
                     arrays.append(o)
-            elif o is not None and not np.isscalar(o):
+            elif isinstance(o, (list, tuple)):  # array-likes that cannot be frozen
                 self.snapshots.append((o, np.array(o, copy=True)))
         for a in arrays:
             _freeze(a)

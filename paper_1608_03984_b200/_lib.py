@@ -132,6 +132,9 @@ EXPORTS = (
      (ctypes.POINTER(AcousticArgs), ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t, _vp)),
     ("fdr_last_launch_count", ctypes.c_int64, ()),
     ("fdr_pending_error", ctypes.c_int, ()),
+    ("fdr_fp32_fma_peak", ctypes.c_int,
+     (ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+      ctypes.POINTER(ctypes.c_double))),
     ("fdr_count_nonfinite", ctypes.c_int,
      (_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
       ctypes.POINTER(ctypes.c_int64), _vp)),

@@ -118,6 +118,38 @@ def cmd_bench(args):
     return 0
 
 
+def cmd_point(args):
+    """Place a measured rate of any catalogue equation on a machine's roofline
+    (the reference's `oi` / `predict` view for one equation, with a measured
+    point): TTI and elastic-VS included (roofline.EQUATIONS, --equations-file)."""
+    from . import charts
+    from . import roofline as RL
+
+    reg = _registry(args)
+    if args.machine not in reg:
+        raise FdroofError(f"unknown machine {args.machine!r}; known: {sorted(reg)}")
+    machine = reg[args.machine]
+    eqs = dict(RL.EQUATIONS)
+    for path in args.equations_file:
+        eqs.update(RL.load_equations(path))
+    if args.equation not in eqs:
+        raise FdroofError(f"unknown equation {args.equation!r}; known: {sorted(eqs)}")
+    eq = eqs[args.equation]
+    pt = RL.equation_point(machine, eq, args.k, measured_gpts=args.gpts)
+    print(f"equation:          {eq.name} (k={args.k})")
+    print(f"flops/point:       {RL.kernel_flops(eq, args.k)}")
+    print(f"bytes/point:       {RL.equation_bytes_per_point(eq, machine.precision_bytes)}")
+    print(f"oi:                {fmt(pt.oi)} FLOPs/byte")
+    print(f"attainable:        {fmt(pt.attainable_gflops)} GFLOPS on {machine.name} ({pt.bound}-bound)")
+    if args.gpts is not None:
+        print(f"measured:          {fmt(pt.measured_gflops)} GFLOPS ({fmt(args.gpts)} GPts/s)")
+        print(f"of attainable:     {pt.fraction * 100.0:.1f}%")
+    if args.svg:
+        charts.write_svg(charts.roofline_chart(RL.roofline_dataset(machine, (pt,))), args.svg)
+        print(f"wrote {args.svg}")
+    return 0
+
+
 def build_parser():
     p = argparse.ArgumentParser(prog="paper_1608_03984_b200",
                                 description="B200 time stepping for the fdroof acoustic kernel")
@@ -139,6 +171,14 @@ def build_parser():
     sp.add_argument("--dump", metavar="PATH")
     sp.add_argument("--variant", default="auto", choices=("auto", "queue", "tma", "direct"))
     sp.set_defaults(func=cmd_bench)
+    sp = sub.add_parser("point", help="one equation's roofline point (TTI, elastic-vs, ...)")
+    sp.add_argument("--equation", required=True)
+    sp.add_argument("--k", type=int, default=9, help="stencil points per line (order + 1)")
+    sp.add_argument("--machine", required=True)
+    sp.add_argument("--gpts", type=float, help="measured grid-point updates per second (1e9)")
+    sp.add_argument("--equations-file", action="append", default=[], metavar="PATH")
+    sp.add_argument("--svg")
+    sp.set_defaults(func=cmd_point)
     return p
 
 

@@ -353,7 +353,7 @@ class _DevicePlan:
 
     def __init__(self, cfg: KernelConfig, device, pitch: int):
         torch = _torch()
-        self.key = _plan_key(cfg, device)
+        self.key = _plan_key(cfg, device, pitch)
         self.guard = InputGuard(config_inputs(cfg, ("m",)))  # frozen while cached
         nx, ny, nz = cfg.dims
         self.weights = acoustic_weights_f32(cfg.order)

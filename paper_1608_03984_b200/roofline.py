@@ -252,6 +252,120 @@ def roofline_point(machine: MachineSpec, order: int,
                          measured_gflops)
 
 
+# ------------------------------------------------------------ equations
+# The reference's cost catalogue schema (equations.py:20-101, the equations
+# YAML hook at :218-246) for the kernels this package time-steps, so the report
+# front end can place TTI (config 4) and the elastic velocity-stress system
+# (config 5) on the roofline next to the acoustic kernel.
+
+
+@dataclass(frozen=True)
+class EquationSpec:
+    """fdroof.equations.EquationSpec: per-point FLOPs from derivative counts
+    (or a fixed count) and the field values moved per point per step."""
+
+    name: str
+    factor: int = 1
+    n_first: int = 0
+    n_second: int = 0
+    n_cross: int = 0
+    extra_mult: int = 0
+    extra_add: int = 0
+    duplicates: int = 0
+    fields_moved: int = 1
+    fixed_kernel_flops: Optional[int] = None
+    description: str = ""
+
+    def __post_init__(self):
+        if not self.name:
+            raise ValidationError("equation name must be non-empty")
+        if self.factor < 1:
+            raise ValidationError(f"{self.name}: factor must be >= 1")
+        for attr in ("n_first", "n_second", "n_cross", "extra_mult", "extra_add", "duplicates"):
+            if getattr(self, attr) < 0:
+                raise ValidationError(f"{self.name}: {attr} must be >= 0")
+        if self.fields_moved < 1:
+            raise ValidationError(f"{self.name}: fields_moved must be >= 1")
+        if self.fixed_kernel_flops is not None and self.fixed_kernel_flops < 1:
+            raise ValidationError(f"{self.name}: fixed_kernel_flops must be >= 1")
+
+
+def kernel_flops(eq: EquationSpec, k: int) -> int:
+    """equations.py:55-71: axis derivatives 2k FLOPs, cross derivatives
+    2k^2 - 4k - 1 (stencils.py:116-128), plus the extras, minus duplicates,
+    times the coupled-system factor; or the fixed count."""
+    if eq.fixed_kernel_flops is not None:
+        return eq.fixed_kernel_flops
+    if k < 2:
+        raise ValidationError(f"stencil size k must be >= 2, got {k}")
+    per = ((eq.n_first + eq.n_second) * 2 * k + eq.n_cross * (2 * k * k - 4 * k - 1)
+           + eq.extra_mult + eq.extra_add - eq.duplicates)
+    return eq.factor * per
+
+
+def equation_bytes_per_point(eq: EquationSpec, precision_bytes: int = 4) -> int:
+    return eq.fields_moved * precision_bytes
+
+
+EQUATIONS = {e.name: e for e in (
+    EquationSpec("acoustic", factor=1, n_second=3, extra_mult=3, extra_add=5, duplicates=4,
+                 fields_moved=4, description="the reference's acoustic entry (equations.py:122-132)"),
+    EquationSpec("tti", factor=2, n_second=3, n_cross=3, extra_mult=44, extra_add=17,
+                 duplicates=8, fields_moved=15,
+                 description="the reference's TTI catalogue entry (equations.py:144-155): "
+                             "964 FLOPs at k = 9, 60 B/pt"),
+    # the kernels built here, with the FLOPs they execute per point (ncu:
+    # FADD/FMUL 1, FFMA/FADD2/FMUL2 2, FFMA2 4; profiles/r02_ncu_flops.json)
+    EquationSpec("tti-b200", fixed_kernel_flops=242, fields_moved=15,
+                 description="tti_pack (csrc/tti.cu): p and r in f32x2 lanes, shared derivative "
+                             "chains; ncu-counted FLOPs at order 8; 9 parameters + 2x2 levels "
+                             "read, p and r written"),
+    EquationSpec("elastic-vs", fixed_kernel_flops=248, fields_moved=21,
+                 description="isotropic velocity-stress (csrc/elastic.cu, SURVEY.md §8(a')): 9 "
+                             "fields read and written, buoyancy / lambda / mu read (infinite-cache "
+                             "traffic, equations.py:7-8); ncu-counted FLOPs at order 8 (velocity "
+                             "115.5 + stress 132.5)"),
+)}
+
+_EQ_KEYS = {"name", "factor", "n_first", "n_second", "n_cross", "extra_mult", "extra_add",
+            "duplicates", "fields_moved", "fixed_kernel_flops", "description", "override"}
+
+
+def load_equations(path) -> dict:
+    """Equation documents of a YAML file (one per document), the reference's
+    hook (equations.py:218-246): shadowing a built-in needs `override: true`."""
+    import yaml
+
+    with open(path, encoding="utf-8") as fh:
+        docs = [d for d in yaml.safe_load_all(fh) if d is not None]
+    out = {}
+    for d in docs:
+        if not isinstance(d, dict) or "name" not in d:
+            raise ValidationError(f"{path}: equation document must be a mapping with a name")
+        unknown = set(d) - _EQ_KEYS
+        if unknown:
+            raise ValidationError(f"{path}: unknown equation keys: {sorted(unknown)}")
+        eq = EquationSpec(**{k: v for k, v in d.items() if k != "override"})
+        if eq.name in EQUATIONS and not d.get("override", False):
+            raise ValidationError(f"{path}: '{eq.name}' is a built-in equation; "
+                                  "set 'override: true' to replace it")
+        out[eq.name] = eq
+    return out
+
+
+def equation_point(machine: MachineSpec, eq: EquationSpec, k: int,
+                   measured_gpts: Optional[float] = None,
+                   label: Optional[str] = None) -> RooflinePoint:
+    """The roofline point of any catalogue equation: OI = kernel_flops /
+    bytes, attainable = min(OI B, F); a measured rate in grid points per
+    second is converted with the same FLOP count (analysis.py:170-181)."""
+    fl = kernel_flops(eq, k)
+    oi = fl / equation_bytes_per_point(eq, machine.precision_bytes)
+    bound = "memory" if oi < machine.ridge_point else "compute"
+    meas = None if measured_gpts is None else measured_gpts * fl
+    return RooflinePoint(label or f"{eq.name}:k{k}", oi, machine.attainable(oi), bound, k, meas)
+
+
 @dataclass(frozen=True)
 class RooflineDataset:
     """A machine's roof plus the points pinned against it (analysis.py:123-167)."""

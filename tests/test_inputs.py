@@ -95,3 +95,17 @@ def test_readonly_input_left_readonly():
     _get(cfg)
     invalidate_plan(cfg)
     assert not cfg.m.flags.writeable
+
+
+def test_device_plan_reused_across_runs():
+    """The plan key must be stable between calls: a rebuild per call would
+    re-upload m every run (and every step() call)."""
+    import torch
+
+    from paper_1608_03984_b200 import kernel as K
+
+    cfg = _cfg()
+    p = K._plan(cfg, torch.device("cpu"), 8)
+    assert K._plan(cfg, torch.device("cpu"), 8) is p
+    assert K._plan(cfg, torch.device("cpu"), 12) is not p  # another pitch: another layout
+    invalidate_plan(cfg)
