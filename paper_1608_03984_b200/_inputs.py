@@ -144,3 +144,25 @@ def host_tensor(a):
     with warnings.catch_warnings():
         warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
         return torch.from_numpy(a)
+
+
+def grow_traces(fld, rows, n_rec, dtype, device):
+    """A (rows, n_rec) trace view for `fld`, keeping the rows recorded so far.
+    The backing store grows geometrically, so a step()-per-call loop that runs
+    past cfg.n_t (one more row per call) copies O(rows) in total, not O(rows^2)."""
+    import torch
+
+    store = getattr(fld, "_trace_store", None)
+    old = fld.traces
+    if store is None or store.shape[1] != n_rec or store.dtype != dtype or store.shape[0] < rows:
+        cap = rows if store is None or store.shape[1] != n_rec else max(rows, 2 * int(store.shape[0]))
+        new = torch.zeros((cap, n_rec), dtype=dtype, device=device)
+        if old is not None and old.shape[1] == n_rec:
+            new[: old.shape[0]].copy_(old)
+        store = new
+        fld._trace_store = store
+    elif old is None or old.data_ptr() != store.data_ptr():
+        store.zero_()
+        if old is not None and old.shape[1] == n_rec:
+            store[: old.shape[0]].copy_(old)
+    return store[:rows]

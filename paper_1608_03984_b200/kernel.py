@@ -23,7 +23,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._inputs import InputGuard, cached_plan, config_inputs, host_tensor, invalidate_plan  # noqa: F401
+from ._inputs import InputGuard, cached_plan, config_inputs, grow_traces, host_tensor, invalidate_plan  # noqa: F401
 from .errors import ValidationError
 from .roofline import (
     ACOUSTIC_BYTES_PER_POINT,
@@ -483,10 +483,7 @@ def run(fld: Wavefield, cfg: KernelConfig, n_steps: Optional[int] = None,
         rows = max(cfg.n_t, fld.it + n)
         n_rec = cfg.receivers.count
         if fld.traces is None or fld.traces.shape[1] != n_rec or fld.traces.shape[0] < rows:
-            grown = torch.zeros((rows, n_rec), dtype=torch.float32, device=dev)
-            if fld.traces is not None and fld.traces.shape[1] == n_rec:
-                grown[: fld.traces.shape[0]].copy_(fld.traces)
-            fld.traces = grown
+            fld.traces = grow_traces(fld, rows, n_rec, torch.float32, dev)
         args.rec_xyz = plan.rec.data_ptr()
         args.traces = fld.traces.data_ptr()
         args.trace_rows = int(fld.traces.shape[0])
@@ -575,10 +572,9 @@ def _run_f64(fld: Wavefield, cfg: KernelConfig, n: int, variant: str) -> Wavefie
         rows = max(cfg.n_t, fld.it + n)
         if fld.traces is None or fld.traces.dtype != torch.float64 or fld.traces.shape[0] < rows \
                 or fld.traces.shape[1] != a.n_rec:
-            grown = torch.zeros((rows, a.n_rec), dtype=torch.float64, device=dev)
-            if fld.traces is not None and fld.traces.shape[1] == a.n_rec:
-                grown[: fld.traces.shape[0]].copy_(fld.traces)
-            fld.traces = grown
+            if fld.traces is not None and fld.traces.dtype != torch.float64:
+                fld.traces = None
+            fld.traces = grow_traces(fld, rows, a.n_rec, torch.float64, dev)
         a.rec_xyz = plan.rec.data_ptr()
         a.traces = fld.traces.data_ptr()
         a.trace_rows = int(fld.traces.shape[0])

@@ -27,7 +27,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._inputs import InputGuard, cached_plan, config_inputs, host_tensor
+from ._inputs import InputGuard, cached_plan, config_inputs, grow_traces, host_tensor
 from .errors import ValidationError
 from .kernel import Receivers, Source, Sponge, StabilityWarning, row_pitch
 from .stencils import first_derivative_weights, second_derivative_weights
@@ -291,11 +291,8 @@ def tti_run(fld: TTIWavefield, cfg: TTIConfig, n_steps: Optional[int] = None,
     if plan.rec is not None:
         rows = max(cfg.n_t, fld.it + n)
         n_rec = cfg.receivers.count
-        if fld.traces is None or fld.traces.shape[0] < rows:
-            grown = torch.zeros((rows, n_rec), dtype=torch.float32, device=dev)
-            if fld.traces is not None:
-                grown[: fld.traces.shape[0]].copy_(fld.traces)
-            fld.traces = grown
+        if fld.traces is None or fld.traces.shape[0] < rows or fld.traces.shape[1] != n_rec:
+            fld.traces = grow_traces(fld, rows, n_rec, torch.float32, dev)
         a.n_rec = n_rec
         a.rec_xyz = plan.rec.data_ptr()
         a.traces = fld.traces.data_ptr()

@@ -109,3 +109,26 @@ def test_device_plan_reused_across_runs():
     assert K._plan(cfg, torch.device("cpu"), 8) is p
     assert K._plan(cfg, torch.device("cpu"), 12) is not p  # another pitch: another layout
     invalidate_plan(cfg)
+
+
+def test_trace_store_grows_geometrically():
+    import torch
+
+    from paper_1608_03984_b200._inputs import grow_traces
+
+    class F:
+        traces = None
+
+    f = F()
+    f.traces = grow_traces(f, 4, 3, torch.float32, "cpu")
+    f.traces[:] = 1.0
+    allocs = set()
+    for rows in range(5, 200):
+        f.traces = grow_traces(f, rows, 3, torch.float32, "cpu")
+        allocs.add(f._trace_store.data_ptr())
+        assert f.traces.shape == (rows, 3) and f.traces.is_contiguous()
+        assert (f.traces[:4] == 1.0).all() and (f.traces[4:] == 0.0).all()
+    assert len(allocs) <= 7  # doublings, not one allocation per row
+    f.traces = None  # a reset starts from zeros again
+    f.traces = grow_traces(f, 10, 3, torch.float32, "cpu")
+    assert (f.traces == 0).all()
