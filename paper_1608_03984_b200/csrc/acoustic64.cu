@@ -551,18 +551,11 @@ template <int R, bool GRID_M, bool SPONGE>
 static int queue_inst(const A64Step& s, const Maps64& mp, int k, cudaStream_t st, int* chunk_cache) {
   using G = QG64<R>;
   auto kern = a64_queue<R, GRID_M, SPONGE>;
-  static int cfg_dev = -1, occ = 1, nsm = 148;
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  if (cfg_dev != dev) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, QNT, G::SMEM);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return cuda_fail(e, "a64_queue setup");
-    if (occ < 1) return fail(FDR_ECUDA, "float64 queue kernel (r=%d) cannot be resident", R);
-    cfg_dev = dev;
-  }
+  // occupancy facts per (kernel, device), cached under a lock (concurrent
+  // callers on several devices share launch_facts' table)
+  int occ = 0, nsm = 0;
+  const int frc = fdr::launch_facts(reinterpret_cast<const void*>(kern), QNT, G::SMEM, &occ, &nsm);
+  if (frc != FDR_OK) return frc;
   const int tzn = (s.nz + QTZ - 1) / QTZ, tyn = (s.ny + QTY - 1) / QTY;
   if (*chunk_cache <= 0) {
     const long tiles = (long)tzn * tyn, slots = (long)occ * nsm;
@@ -585,7 +578,7 @@ static int queue_inst(const A64Step& s, const Maps64& mp, int k, cudaStream_t st
   const int cur = (2 + k) % 3, prev = (1 + k) % 3;
   dim3 grid(tzn, tyn, (s.nx + t.chunk - 1) / t.chunk);
   kern<<<grid, QNT, G::SMEM, st>>>(mp.box[cur], mp.tile[cur], mp.tile[prev], mp.m, t);
-  e = cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? FDR_OK : cuda_fail(e, "a64_queue launch");
 }
 

@@ -526,15 +526,8 @@ static int el_encode(CUtensorMap* map, const float* base, const fdr_elastic_args
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                           CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                           CUtensorMapFloatOOBfill);
-  static Enc enc = nullptr;
-  if (!enc) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return fail(FDR_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    enc = reinterpret_cast<Enc>(p);
-  }
+  const Enc enc = reinterpret_cast<Enc>(fdr::tensor_map_encoder());
+  if (!enc) return fail(FDR_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)a->nz, (cuuint64_t)a->ny, (cuuint64_t)a->nx};
   cuuint64_t strides[2] = {(cuuint64_t)a->pitch_y * 4, (cuuint64_t)a->pitch_x * 4};
   cuuint32_t box[3] = {(cuuint32_t)bz, (cuuint32_t)by, 1}, es[3] = {1, 1, 1};

@@ -27,6 +27,10 @@ int cuda_fail(cudaError_t e, const char* what);
 // devices never see another device's answer.  FDR_OK or an error code.
 int launch_facts(const void* kern, int threads, size_t smem, int* occ, int* nsm);
 
+// The driver's cuTensorMapEncodeTiled, resolved once under std::call_once
+// (safe from concurrent host threads); nullptr when the driver lacks it.
+void* tensor_map_encoder();
+
 // lap + w * (a + b): one tap pair of kernel.py:205 (three roundings).
 FDR_DEV float tap(float lap, float w, float a, float b) {
   return __fadd_rn(lap, __fmul_rn(w, __fadd_rn(a, b)));
