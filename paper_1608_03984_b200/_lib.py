@@ -15,7 +15,7 @@ LIB_NAME = "libb200fd.so"
 LIB_PATH = os.environ.get("B200FD_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 MAX_RADIUS = 16
 
 FDR_OK, FDR_EINVAL, FDR_ECUDA = 0, -1, -2

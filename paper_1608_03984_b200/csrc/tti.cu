@@ -52,11 +52,12 @@ struct TTIStep {
   float* traces;
   int gather_row;
   int gather_pad_chunk;  // x-planes per CTA (stream kernel)
+  int es;                // floats between consecutive points: 1 separate p/r, 2 interleaved
 };
 
 __device__ __forceinline__ float at(const float* u, const TTIStep& a, int x, int y, int z) {
   if (x < 0 || x >= a.nx || y < 0 || y >= a.ny || z < 0 || z >= a.nz) return 0.0f;
-  return u[(size_t)x * a.pitch_x + (size_t)y * a.pitch_y + z];
+  return u[a.es * ((size_t)x * a.pitch_x + (size_t)y * a.pitch_y + z)];
 }
 
 // first derivative along axis `ax` (0 x, 1 y, 2 z) at (x, y, z)
@@ -110,7 +111,7 @@ __device__ void gather(const TTIStep& a) {
   for (int i = b * nthr + t; i < a.n_rec; i += stride) {
     const int* c = a.rec + 3 * i;
     a.traces[(size_t)a.gather_row * a.n_rec + i] =
-        a.p[(size_t)c[0] * a.pitch_x + (size_t)c[1] * a.pitch_y + c[2]];
+        a.p[a.es * ((size_t)c[0] * a.pitch_x + (size_t)c[1] * a.pitch_y + c[2])];
   }
 }
 
@@ -122,14 +123,15 @@ __global__ void __launch_bounds__(256) tti_direct(const TTIStep a) {
   const int x = blockIdx.z;
   if (z >= a.nz || y >= a.ny) return;
   const size_t o = (size_t)x * a.pitch_x + (size_t)y * a.pitch_y + z;
+  const size_t e = (size_t)a.es * o;  // level element of the point
   const float k = a.prm[0][o], pa = a.prm[1][o], pb = a.prm[2][o];
   const float c[6] = {a.prm[3][o], a.prm[4][o], a.prm[5][o], a.prm[6][o], a.prm[7][o], a.prm[8][o]};
   float Gp, Lp, Gr, Lr;
   gl_op(a.p, a, x, y, z, c, &Gp, &Lp);
   gl_op(a.r, a, x, y, z, c, &Gr, &Lr);
   const float Hp = __fsub_rn(Lp, Gp);
-  float pn = __fmaf_rn(k, __fmaf_rn(pa, Hp, __fmul_rn(pb, Gr)), __fmaf_rn(2.0f, a.p[o], -a.pp[o]));
-  float rn = __fmaf_rn(k, __fmaf_rn(pb, Hp, Gr), __fmaf_rn(2.0f, a.r[o], -a.rp[o]));
+  float pn = __fmaf_rn(k, __fmaf_rn(pa, Hp, __fmul_rn(pb, Gr)), __fmaf_rn(2.0f, a.p[e], -a.pp[e]));
+  float rn = __fmaf_rn(k, __fmaf_rn(pb, Hp, Gr), __fmaf_rn(2.0f, a.r[e], -a.rp[e]));
   if (a.gx) {
     const float g = __fmul_rn(__fmul_rn(a.gx[x], a.gy[y]), a.gz[z]);
     pn = __fmul_rn(pn, g);
@@ -139,16 +141,16 @@ __global__ void __launch_bounds__(256) tti_direct(const TTIStep a) {
     pn = __fadd_rn(pn, a.series[a.it]);
     rn = __fadd_rn(rn, a.series[a.it]);
   }
-  a.pn[o] = pn;
-  a.rn[o] = rn;
+  a.pn[e] = pn;
+  a.rn[e] = rn;
 }
 
 __global__ void tti_gather_kernel(const float* p, const int* rec, int n_rec, float* traces, int row,
-                                  int pitch_y, long long pitch_x) {
+                                  int pitch_y, long long pitch_x, int es) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n_rec) {
     const int* c = rec + 3 * i;
-    traces[(size_t)row * n_rec + i] = p[(size_t)c[0] * pitch_x + (size_t)c[1] * pitch_y + c[2]];
+    traces[(size_t)row * n_rec + i] = p[es * ((size_t)c[0] * pitch_x + (size_t)c[1] * pitch_y + c[2])];
   }
 }
 
@@ -479,6 +481,16 @@ constexpr bool TTI_CARRY = FDR_TTI_CARRY != 0;
 constexpr bool TTI_CARRY = true;
 #endif
 
+// D1z of an interleaved (p, r) row from the 32-bit shared address of the
+// own pair: one 8-byte load per tap
+template <int R>
+FDR_DEV f2 d1_row2i(uint32_t hp, const float* w1) {
+  f2 d = mul2(bcast(w1[1]), sub2(lds64a(hp + 8), lds64a(hp - 8)));
+#pragma unroll
+  for (int j = 2; j <= R; ++j) d = fma2(bcast(w1[j]), sub2(lds64a(hp + 8 * j), lds64a(hp - 8 * j)), d);
+  return d;
+}
+
 template <int R>
 FDR_DEV f2 d1_row2(const float* hp, const float* hr, const float* w1) {  // D1z, both fields
   f2 d = mul2(bcast(w1[1]), sub2(ldpr(hp, hr, 1), ldpr(hp, hr, -1)));
@@ -487,7 +499,7 @@ FDR_DEV f2 d1_row2(const float* hp, const float* hr, const float* w1) {  // D1z,
   return d;
 }
 
-template <int R, bool SPONGE>
+template <int R, bool SPONGE, bool IL>
 __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ TTIMaps maps,
                                                        const TTIStep a) {
   using G = TGeo<R>;
@@ -513,8 +525,12 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
     const bool cen = p >= 2 * R;
     const uint32_t bytes = 2 * G::BOX_BYTES + 3 * G::TILE * 4 + (cen ? 8 * G::TILE * 4 : 0);
     mbar_arrive_expect_tx(&full[s], bytes);
-    tma_load_3d(st + G::O_BP, &maps.box_p, &full[s], zt - G::LZ, yt - R, xn);
-    tma_load_3d(st + G::O_BR, &maps.box_r, &full[s], zt - G::LZ, yt - R, xn);
+    if (IL) {  // one box of (p, r) pairs: twice the z extent in floats
+      tma_load_3d(st + G::O_BP, &maps.box_p, &full[s], 2 * (zt - G::LZ), yt - R, xn);
+    } else {
+      tma_load_3d(st + G::O_BP, &maps.box_p, &full[s], zt - G::LZ, yt - R, xn);
+      tma_load_3d(st + G::O_BR, &maps.box_r, &full[s], zt - G::LZ, yt - R, xn);
+    }
     tma_load_3d(st + G::O_IN + 0 * G::TILE, &maps.prm[4], &full[s], zt, yt, xn);  // cyy
     tma_load_3d(st + G::O_IN + 1 * G::TILE, &maps.prm[5], &full[s], zt, yt, xn);  // czz
     tma_load_3d(st + G::O_IN + 2 * G::TILE, &maps.prm[7], &full[s], zt, yt, xn);  // cyz
@@ -524,13 +540,17 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
 #pragma unroll
       for (int i = 0; i < 6; ++i)
         tma_load_3d(st + G::O_CEN + i * G::TILE, &maps.prm[src[i]], &full[s], zt, yt, xc);
-      tma_load_3d(st + G::O_CEN + 6 * G::TILE, &maps.prev_p, &full[s], zt, yt, xc);
-      tma_load_3d(st + G::O_CEN + 7 * G::TILE, &maps.prev_r, &full[s], zt, yt, xc);
+      if (IL) {  // (p, r) pairs of the previous level
+        tma_load_3d(st + G::O_CEN + 6 * G::TILE, &maps.prev_p, &full[s], 2 * zt, yt, xc);
+      } else {
+        tma_load_3d(st + G::O_CEN + 6 * G::TILE, &maps.prev_p, &full[s], zt, yt, xc);
+        tma_load_3d(st + G::O_CEN + 7 * G::TILE, &maps.prev_r, &full[s], zt, yt, xc);
+      }
     }
   };
   if (tid == 0) {
     prefetch_tensormap(&maps.box_p);
-    prefetch_tensormap(&maps.box_r);
+    if (!IL) prefetch_tensormap(&maps.box_r);
     for (int s = 0; s < G::NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], G::NWARPS);
@@ -578,9 +598,10 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
   constexpr bool CA = TTI_CARRY;
   constexpr uint32_t SB = G::STAGE * 4u, DR = (G::O_BR - G::O_BP) * 4u;
   const int hr0 = hrow >= 0 ? hrow : 0;
-  uint32_t ab = smem_u32(smem + G::O_BP + bown), at = smem_u32(smem + town);
+  // IL: (p, r) pairs, the own point at float 2 * bown of the box
+  uint32_t ab = smem_u32(smem + G::O_BP + (IL ? 2 : 1) * bown), at = smem_u32(smem + town);
   uint32_t adz = smem_u32(smem + G::O_DZP + 2 * ((ty + R) * TTZ + tz));
-  uint32_t ah = smem_u32(smem + G::O_BP + hr0 * G::BZ + G::LZ + tz);
+  uint32_t ah = smem_u32(smem + G::O_BP + (IL ? 2 : 1) * (hr0 * G::BZ + G::LZ + tz));
   uint32_t ahdz = smem_u32(smem + G::O_DZP + 2 * (hr0 * TTZ + tz));
   uint32_t af = smem_u32(full);  // full[slot]; empty[] and dzrdy[] follow
 #pragma unroll 1
@@ -591,7 +612,10 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
       if (p >= nplanes) break;
       if (CA) mbar_wait_a(af, phase); else mbar_wait(&full[slot], phase);
       float* st = smem + slot * G::STAGE;
-      auto lp = [&](int off) { return CA ? ldpra(ab, DR, off) : ldpr(st + G::O_BP + bown, st + G::O_BR + bown, off); };
+      auto lp = [&](int off) -> f2 {
+        if (IL) return CA ? lds64a(ab + 8 * off) : *reinterpret_cast<const f2*>(st + G::O_BP + 2 * (bown + off));
+        return CA ? ldpra(ab, DR, off) : ldpr(st + G::O_BP + bown, st + G::O_BR + bown, off);
+      };
       auto lt = [&](int off) { return CA ? lds32a(at + 4 * off) : st[town + off]; };
       // ---- in-plane work on the newest plane, both fields packed
       const f2 uo = lp(0);
@@ -614,12 +638,13 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
       float* dzb = st + G::O_DZP;  // interleaved (p, r) D1z rows, 2 * BY * TTZ floats
       if (CA) {
         sts64a(adz, dz1);
-        if (hrow >= 0) sts64a(ahdz, d1_row2a<R>(ah, DR, a.w1));
+        if (hrow >= 0) sts64a(ahdz, IL ? d1_row2i<R>(ah, a.w1) : d1_row2a<R>(ah, DR, a.w1));
       } else {
         *reinterpret_cast<f2*>(dzb + 2 * ((ty + R) * TTZ + tz)) = dz1;
         if (hrow >= 0)
           *reinterpret_cast<f2*>(dzb + 2 * (hrow * TTZ + tz)) =
-              d1_row2<R>(st + G::O_BP + hrow * G::BZ + G::LZ + tz, st + G::O_BR + hrow * G::BZ + G::LZ + tz, a.w1);
+              IL ? d1_row2i<R>(smem_u32(st + G::O_BP + 2 * (hrow * G::BZ + G::LZ + tz)), a.w1)
+                 : d1_row2<R>(st + G::O_BP + hrow * G::BZ + G::LZ + tz, st + G::O_BR + hrow * G::BZ + G::LZ + tz, a.w1);
       }
       qu[2 * R + u] = uo;
       qy[2 * R + u] = dy1;
@@ -641,7 +666,16 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
         const float vk = lt(G::O_CEN), va = lt(G::O_CEN + G::TILE), vb = lt(G::O_CEN + 2 * G::TILE);
         const float cxx = lt(G::O_CEN + 3 * G::TILE), cxy = lt(G::O_CEN + 4 * G::TILE);
         const float cxz = lt(G::O_CEN + 5 * G::TILE);
-        const float ppv = lt(G::O_CEN + 6 * G::TILE), rpv = lt(G::O_CEN + 7 * G::TILE);
+        float ppv, rpv;
+        if (IL) {  // one 8-byte load of the (p, r) pair
+          const f2 pr = CA ? lds64a(at + 4u * (G::O_CEN + 6 * G::TILE + town))
+                           : *reinterpret_cast<const f2*>(st + G::O_CEN + 6 * G::TILE + 2 * town);
+          ppv = lo(pr);
+          rpv = hi(pr);
+        } else {
+          ppv = lt(G::O_CEN + 6 * G::TILE);
+          rpv = lt(G::O_CEN + 7 * G::TILE);
+        }
         const int c = u + R;
         f2 dxx = mul2(bcast(a.w2[0]), qu[c]);
         f2 dxy = mul2(bcast(a.w1[1]), sub2(qy[c + 1], qy[c - 1]));
@@ -672,8 +706,12 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
         }
         if (ok) {
           const uint32_t o = oidx0 + (uint32_t)k * px32;
-          a.pn[o] = pn;
-          a.rn[o] = rn;
+          if (IL) {
+            asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(a.pn + 2u * o), "f"(pn), "f"(rn) : "memory");
+          } else {
+            a.pn[o] = pn;
+            a.rn[o] = rn;
+          }
         }
       }
       // the D1z rows are complete
@@ -721,18 +759,20 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
   }
 }
 
-static int tti_encode(CUtensorMap* map, const float* base, const fdr_tti_args* a, int bz, int by) {
+static int tti_encode(CUtensorMap* map, const float* base, const fdr_tti_args* a, int bz, int by,
+                      int es = 1) {
   typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                           CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                           CUtensorMapFloatOOBfill);
   const Enc enc = reinterpret_cast<Enc>(fdr::tensor_map_encoder());
   if (!enc) return fail(FDR_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)a->nz, (cuuint64_t)a->ny, (cuuint64_t)a->nx};
-  cuuint64_t strides[2] = {(cuuint64_t)a->pitch_y * 4, (cuuint64_t)a->pitch_x * 4};
-  cuuint32_t box[3] = {(cuuint32_t)bz, (cuuint32_t)by, 1}, es[3] = {1, 1, 1};
+  // es = 2: (p, r) pairs, i.e. a tensor with twice the z extent in floats
+  cuuint64_t dims[3] = {(cuuint64_t)a->nz * es, (cuuint64_t)a->ny, (cuuint64_t)a->nx};
+  cuuint64_t strides[2] = {(cuuint64_t)a->pitch_y * 4 * es, (cuuint64_t)a->pitch_x * 4 * es};
+  cuuint32_t box[3] = {(cuuint32_t)(bz * es), (cuuint32_t)by, 1}, els[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
-                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   box, els, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FDR_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return FDR_OK;
@@ -743,17 +783,27 @@ static int stream_inst(const TTIStep& s, const fdr_tti_args* a, int k, cudaStrea
                        int* chunk_cache) {
   using G = TGeo<R>;
   const bool sponge = s.gx != nullptr;
-  auto kern = PACK ? (sponge ? tti_pack<R, true> : tti_pack<R, false>)
+  const bool il = a->interleaved != 0;
+  auto kern = PACK ? (il ? (sponge ? tti_pack<R, true, true> : tti_pack<R, false, true>)
+                         : (sponge ? tti_pack<R, true, false> : tti_pack<R, false, false>))
                    : (sponge ? tti_stream<R, true> : tti_stream<R, false>);
   int occ = 0, nsm = 0;
   const int frc = fdr::launch_facts(reinterpret_cast<const void*>(kern), TNT, G::SMEM, &occ, &nsm);
   if (frc != FDR_OK) return frc;
   TTIMaps maps;
   const int cur = (2 + k) % 3, prev = (1 + k) % 3;
-  int rc = tti_encode(&maps.box_p, a->p[cur], a, G::BZ, G::BY);
-  if (rc == FDR_OK) rc = tti_encode(&maps.box_r, a->r[cur], a, G::BZ, G::BY);
-  if (rc == FDR_OK) rc = tti_encode(&maps.prev_p, a->p[prev], a, TTZ, TTY);
-  if (rc == FDR_OK) rc = tti_encode(&maps.prev_r, a->r[prev], a, TTZ, TTY);
+  int rc = FDR_OK;
+  if (il) {  // r[i] == p[i] + 1: the p maps cover the pairs; the r maps are unused
+    rc = tti_encode(&maps.box_p, a->p[cur], a, G::BZ, G::BY, 2);
+    if (rc == FDR_OK) rc = tti_encode(&maps.prev_p, a->p[prev], a, TTZ, TTY, 2);
+    maps.box_r = maps.box_p;
+    maps.prev_r = maps.prev_p;
+  } else {
+    rc = tti_encode(&maps.box_p, a->p[cur], a, G::BZ, G::BY);
+    if (rc == FDR_OK) rc = tti_encode(&maps.box_r, a->r[cur], a, G::BZ, G::BY);
+    if (rc == FDR_OK) rc = tti_encode(&maps.prev_p, a->p[prev], a, TTZ, TTY);
+    if (rc == FDR_OK) rc = tti_encode(&maps.prev_r, a->r[prev], a, TTZ, TTY);
+  }
   for (int i = 0; i < 9 && rc == FDR_OK; ++i) rc = tti_encode(&maps.prm[i], a->params[i], a, TTZ, TTY);
   if (rc != FDR_OK) return rc;
   TTIStep t = s;
@@ -793,7 +843,7 @@ int tti_stream_launch(const TTIStep& s, const fdr_tti_args* a, int k, cudaStream
 }
 
 int tti_stream_prepare(const fdr_tti_args* a) {
-  if ((uint64_t)a->nx * (uint64_t)a->pitch_x >= (1ull << 32))
+  if ((uint64_t)a->nx * (uint64_t)a->pitch_x * (a->interleaved ? 2u : 1u) >= (1ull << 32))
     return fail(FDR_EINVAL, "the TTI stream kernel indexes grids of < 2^32 elements");
   return FDR_OK;
 }
@@ -814,6 +864,14 @@ static int validate(const fdr_tti_args* a) {
   if (a->n_steps < 0 || a->it0 < 0) return fail(FDR_EINVAL, "n_steps and it0 must be >= 0");
   for (int i = 0; i < 3; ++i)
     if (!a->p[i] || !a->r[i]) return fail(FDR_EINVAL, "level pointer NULL");
+  if (a->interleaved != 0 && a->interleaved != 1)
+    return fail(FDR_EINVAL, "interleaved must be 0 or 1, got %d", a->interleaved);
+  if (a->interleaved)
+    for (int i = 0; i < 3; ++i)
+      if (a->r[i] != a->p[i] + 1)
+        return fail(FDR_EINVAL, "interleaved levels need r[i] == p[i] + 1 (level %d)", i);
+  if (a->interleaved && a->variant == FDR_VARIANT_TMA)
+    return fail(FDR_EINVAL, "the TMA (tti_stream) variant takes separate p/r levels (interleaved = 0)");
   for (int i = 0; i < 9; ++i)
     if (!a->params[i]) return fail(FDR_EINVAL, "parameter grid %d is NULL", i);
   if (a->sponge_x && (!a->sponge_y || !a->sponge_z))
@@ -861,6 +919,7 @@ void fill(TTIStep& s, const fdr_tti_args* a, int k) {
   s.traces = a->traces;
   const int row = s.it - 1;
   s.gather_row = (k > 0 && a->n_rec > 0 && a->traces && row < a->trace_rows) ? row : -1;
+  s.es = a->interleaved ? 2 : 1;
 }
 
 static int run(const fdr_tti_args* a, cudaStream_t st) {
@@ -889,7 +948,8 @@ static int run(const fdr_tti_args* a, cudaStream_t st) {
   const int last = a->it0 + a->n_steps - 1;
   if (a->n_steps > 0 && a->n_rec > 0 && a->traces && last < a->trace_rows) {
     tti_gather_kernel<<<(a->n_rec + 255) / 256, 256, 0, st>>>(
-        a->p[(2 + a->n_steps) % 3], a->rec_xyz, a->n_rec, a->traces, last, a->pitch_y, a->pitch_x);
+        a->p[(2 + a->n_steps) % 3], a->rec_xyz, a->n_rec, a->traces, last, a->pitch_y, a->pitch_x,
+        a->interleaved ? 2 : 1);
     TTI_CUDA(cudaGetLastError());
   }
   return (2 + a->n_steps) % 3;

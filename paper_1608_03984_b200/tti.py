@@ -148,23 +148,34 @@ def _torch():
 
 
 class TTIWavefield:
-    """p and r, three HBM levels each ([scratch, prev, cur] like kernel.py:104-116)."""
+    """p and r, three HBM levels each ([scratch, prev, cur] like kernel.py:104-116).
 
-    def __init__(self, halo, p, r, dims, it=0):
+    `interleaved` (the default) stores each level as (p, r) pairs per point
+    in one (nx, ny, pitch, 2) tensor; `p[i]` / `r[i]` are strided views of
+    it, so the packed streaming kernel reads both fields of a tap with one
+    8-byte shared load (fdr_tti_args.interleaved, include/b200fd.h).
+    interleaved=False keeps two separate arrays (the layout tti_stream needs)."""
+
+    def __init__(self, halo, p, r, dims, it=0, interleaved=False):
         self.halo = int(halo)
         self.p = list(p)
         self.r = list(r)
         self._dims = tuple(int(d) for d in dims)
         self.it = int(it)
         self.traces = None
+        self.interleaved = bool(interleaved)
 
     @classmethod
-    def allocate(cls, dims, halo, device=None):
+    def allocate(cls, dims, halo, device=None, interleaved=True):
         torch = _torch()
         _lib.load()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         nx, ny, nz = (int(d) for d in dims)
         shape = (nx, ny, row_pitch(nz))
+        if interleaved:
+            levels = [torch.zeros(shape + (2,), dtype=torch.float32, device=dev) for _ in range(3)]
+            return cls(halo, [t[..., 0] for t in levels], [t[..., 1] for t in levels], (nx, ny, nz),
+                       interleaved=True)
         mk = lambda: [torch.zeros(shape, dtype=torch.float32, device=dev) for _ in range(3)]  # noqa: E731
         return cls(halo, mk(), mk(), (nx, ny, nz))
 
@@ -181,10 +192,17 @@ class TTIWavefield:
         return t[:, :, : self._dims[2]].cpu().numpy().copy()
 
     def nonfinite_count(self, field: str = "p", level: int = 2) -> int:
-        """NaN/inf values of a field's level, counted on the device."""
+        """NaN/inf values of a field's level, counted on the device.
+        Interleaved levels are counted as (p, r) pairs: both fields together."""
         from .kernel import count_nonfinite
 
-        return count_nonfinite((self.p if field == "p" else self.r)[level], self._dims)
+        t = (self.p if field == "p" else self.r)[level]
+        if self.interleaved:
+            nx, ny, nz = self._dims
+            pair = t.as_strided((nx, ny, 2 * t.shape[2]), (t.stride(0), t.stride(1), 1),
+                                t.storage_offset() - (0 if field == "p" else 1))
+            return count_nonfinite(pair, (nx, ny, 2 * nz))
+        return count_nonfinite(t, self._dims)
 
     def set_interior(self, field: str, level: int, values) -> None:
         torch = _torch()
@@ -208,7 +226,7 @@ class _TTIArgs(ctypes.Structure):
         ("src_x", ctypes.c_int32), ("src_y", ctypes.c_int32), ("src_z", ctypes.c_int32),
         ("n_rec", ctypes.c_int32), ("rec_xyz", ctypes.c_void_p), ("traces", ctypes.c_void_p),
         ("trace_rows", ctypes.c_int32), ("it0", ctypes.c_int32), ("n_steps", ctypes.c_int32),
-        ("variant", ctypes.c_int32),
+        ("variant", ctypes.c_int32), ("interleaved", ctypes.c_int32),
     ]
 
 
@@ -300,6 +318,7 @@ def tti_run(fld: TTIWavefield, cfg: TTIConfig, n_steps: Optional[int] = None,
     a.it0 = fld.it
     a.n_steps = n
     a.variant = _VARIANTS[variant]
+    a.interleaved = 1 if fld.interleaved else 0
     stream = torch.cuda.current_stream(dev).cuda_stream
     with torch.cuda.device(dev):
         _lib.check(lib.fdr_tti_run(ctypes.byref(a), ctypes.c_void_p(stream)))

@@ -112,13 +112,16 @@ def tti_mod(cuda_device):
     return tti
 
 
-def _gpu(tti_mod, cfg, variant, n=None):
-    fld = tti_mod.TTIWavefield.allocate(cfg.dims, cfg.halo)
-    tti_mod.tti_run(fld, cfg, n, variant=variant)
+def _gpu(tti_mod, cfg, variant, n=None, interleaved=None):
+    # the TMA variant (tti_stream) takes separate p/r levels; the others run
+    # on the default interleaved (p, r) pairs, "queue_sep" on separate levels
+    il = variant not in ("stream", "queue_sep") if interleaved is None else interleaved
+    fld = tti_mod.TTIWavefield.allocate(cfg.dims, cfg.halo, interleaved=il)
+    tti_mod.tti_run(fld, cfg, n, variant="queue" if variant == "queue_sep" else variant)
     return fld
 
 
-GPU_VARIANTS = ["queue", "stream", "direct"]
+GPU_VARIANTS = ["queue", "queue_sep", "stream", "direct"]
 
 
 @pytest.mark.gpu

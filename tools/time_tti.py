@@ -16,8 +16,8 @@ def main():
     nt = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     cfg = tti.config4(n_t=nt)
     npts = float(np.prod(cfg.dims))
-    for variant in ("queue", "stream"):
-        fld = tti.TTIWavefield.allocate(cfg.dims, cfg.halo)
+    for variant, il in (("queue", True), ("queue", False), ("stream", False)):
+        fld = tti.TTIWavefield.allocate(cfg.dims, cfg.halo, interleaved=il)
         tti.tti_run(fld, cfg, 2, variant=variant)
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -27,7 +27,7 @@ def main():
         e.synchronize()
         ms = s.elapsed_time(e) / nt
         g = npts / ms / 1e6
-        print(json.dumps({"variant": variant, "ms_per_step": round(ms, 4), "gpts": round(g, 2),
+        print(json.dumps({"variant": variant, "interleaved": il, "ms_per_step": round(ms, 4), "gpts": round(g, 2),
                           "gflops_catalog": round(g * tti.tti_flops_per_point(8), 1),
                           "gbs_60B": round(g * 60, 1)}), flush=True)
 
