@@ -204,9 +204,10 @@ struct TGeo {
 #ifdef FDR_TTI_U
   static constexpr int U = FDR_TTI_U;
 #else
-  // planes per unrolled round; after the carried addresses U = 2 measured
-  // 74.0 GPts/s at config 4 against 69.6 (U = 3), 72.3 (U = 1)
-  static constexpr int U = R <= 2 ? 2 * R + 1 : 2;
+  // planes per unrolled round: the whole window period 2R+1, so tti_pack's
+  // windows rotate by renaming (no shifts; measured 81.2 against 78.5 GPts/s
+  // for U = 2 with shifts at config 4, which had beaten U = 1 and U = 3)
+  static constexpr int U = 2 * R + 1;
 #endif
   static constexpr int QW = 2 * R + U;                       // x-window length
   static constexpr int GW = R + U;                           // delayed in-plane window
@@ -475,6 +476,9 @@ FDR_DEV f2 d1_row2a(uint32_t hp, uint32_t dr, const float* w1) {  // D1z, both f
   for (int j = 2; j <= R; ++j) d = fma2(bcast(w1[j]), sub2(ldpra(hp, dr, j), ldpra(hp, dr, -j)), d);
   return d;
 }
+#ifndef FDR_TTI_ROT
+#define FDR_TTI_ROT 1  // rotating windows (config 4: 78.5 -> 81.2 GPts/s)
+#endif
 #ifdef FDR_TTI_CARRY
 constexpr bool TTI_CARRY = FDR_TTI_CARRY != 0;
 #else
@@ -578,14 +582,20 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
   const uint32_t oidx0 = (uint32_t)xb * px32 + (uint32_t)y * (uint32_t)a.pitch_y + (uint32_t)z;
 
   // x windows (u, D1y u, D1z u; lane 0 p, lane 1 r): index i <-> plane p0 - 2R + i
-  f2 qu[G::QW], qy[G::QW], qz[G::QW];
+  // FDR_TTI_ROT: the windows are rings of period 2R+1 walked by a round of
+  // U = 2R+1 planes (pure register renaming, no shifts); otherwise shifted
+  // by U at the end of each round
+  constexpr bool ROT = FDR_TTI_ROT != 0 && G::U == 2 * R + 1;
+  constexpr int PER = 2 * R + 1;
+  constexpr int NQW = ROT ? PER : G::QW, NGW = ROT ? PER : G::GW;
+  f2 qu[NQW], qy[NQW], qz[NQW];
   // delayed in-plane sums: G partial (both fields), L partial (p): plane p0 - R + i
-  f2 gq[G::GW];
-  float pl[G::GW];
+  f2 gq[NGW];
+  float pl[NGW];
 #pragma unroll
-  for (int i = 0; i < G::QW; ++i) qu[i] = qy[i] = qz[i] = 0ull;
+  for (int i = 0; i < NQW; ++i) qu[i] = qy[i] = qz[i] = 0ull;
 #pragma unroll
-  for (int i = 0; i < G::GW; ++i) {
+  for (int i = 0; i < NGW; ++i) {
     gq[i] = 0ull;
     pl[i] = 0.0f;
   }
@@ -646,12 +656,13 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
               IL ? d1_row2i<R>(smem_u32(st + G::O_BP + 2 * (hrow * G::BZ + G::LZ + tz)), a.w1)
                  : d1_row2<R>(st + G::O_BP + hrow * G::BZ + G::LZ + tz, st + G::O_BR + hrow * G::BZ + G::LZ + tz, a.w1);
       }
-      qu[2 * R + u] = uo;
-      qy[2 * R + u] = dy1;
-      qz[2 * R + u] = dz1;
-      pl[R + u] = __fadd_rn(lo(dyy), lo(dzz));
+      auto QI = [](int i) { return ROT ? i % PER : i; };  // window slot (compile-time after unrolling)
+      qu[QI(2 * R + u)] = uo;
+      qy[QI(2 * R + u)] = dy1;
+      qz[QI(2 * R + u)] = dz1;
+      pl[QI(R + u)] = __fadd_rn(lo(dyy), lo(dzz));
       // gin = fma(cyz, dyz, fma(czz, dzz, cyy dyy)): the dyz term follows the barrier
-      gq[R + u] = fma2(bcast(lt(G::O_IN + 1 * G::TILE)), dzz, mul2(bcast(lt(G::O_IN)), dyy));
+      gq[QI(R + u)] = fma2(bcast(lt(G::O_IN + 1 * G::TILE)), dzz, mul2(bcast(lt(G::O_IN)), dyy));
       // Split barrier: announce this warp's D1z rows, update the plane R
       // behind (which needs no D1z row of this plane), then wait for every
       // warp's rows.  The warps' skew is absorbed by useful work instead of a
@@ -677,22 +688,22 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
           rpv = lt(G::O_CEN + 7 * G::TILE);
         }
         const int c = u + R;
-        f2 dxx = mul2(bcast(a.w2[0]), qu[c]);
-        f2 dxy = mul2(bcast(a.w1[1]), sub2(qy[c + 1], qy[c - 1]));
-        f2 dxz = mul2(bcast(a.w1[1]), sub2(qz[c + 1], qz[c - 1]));
+        f2 dxx = mul2(bcast(a.w2[0]), qu[QI(c)]);
+        f2 dxy = mul2(bcast(a.w1[1]), sub2(qy[QI(c + 1)], qy[QI(c - 1)]));
+        f2 dxz = mul2(bcast(a.w1[1]), sub2(qz[QI(c + 1)], qz[QI(c - 1)]));
 #pragma unroll
         for (int j = 1; j <= R; ++j) {
-          dxx = fma2(bcast(a.w2[j]), add2(qu[c + j], qu[c - j]), dxx);
+          dxx = fma2(bcast(a.w2[j]), add2(qu[QI(c + j)], qu[QI(c - j)]), dxx);
           if (j >= 2) {
-            dxy = fma2(bcast(a.w1[j]), sub2(qy[c + j], qy[c - j]), dxy);
-            dxz = fma2(bcast(a.w1[j]), sub2(qz[c + j], qz[c - j]), dxz);
+            dxy = fma2(bcast(a.w1[j]), sub2(qy[QI(c + j)], qy[QI(c - j)]), dxy);
+            dxz = fma2(bcast(a.w1[j]), sub2(qz[QI(c + j)], qz[QI(c - j)]), dxz);
           }
         }
-        const f2 gf = fma2(bcast(cxz), dxz, fma2(bcast(cxy), dxy, fma2(bcast(cxx), dxx, gq[u])));
-        const float Lp = __fadd_rn(pl[u], lo(dxx));
+        const f2 gf = fma2(bcast(cxz), dxz, fma2(bcast(cxy), dxy, fma2(bcast(cxx), dxx, gq[QI(u)])));
+        const float Lp = __fadd_rn(pl[QI(u)], lo(dxx));
         const float Hp = __fsub_rn(Lp, lo(gf));
         const float Gr = hi(gf);
-        const float pc = lo(qu[c]), rc = hi(qu[c]);
+        const float pc = lo(qu[QI(c)]), rc = hi(qu[QI(c)]);
         float pn = __fmaf_rn(vk, __fmaf_rn(va, Hp, __fmul_rn(vb, Gr)), __fmaf_rn(2.0f, pc, -ppv));
         float rn = __fmaf_rn(vk, __fmaf_rn(vb, Hp, Gr), __fmaf_rn(2.0f, rc, -rpv));
         if (SPONGE) {
@@ -724,7 +735,7 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
         f2 dyz = mul2(bcast(a.w1[1]), sub2(ldz(1), ldz(-1)));
 #pragma unroll
         for (int j = 2; j <= R; ++j) dyz = fma2(bcast(a.w1[j]), sub2(ldz(j), ldz(-j)), dyz);
-        gq[R + u] = fma2(bcast(lt(G::O_IN + 2 * G::TILE)), dyz, gq[R + u]);
+        gq[QI(R + u)] = fma2(bcast(lt(G::O_IN + 2 * G::TILE)), dyz, gq[QI(R + u)]);
       }
       // release the stage (every read of it is above)
       __syncwarp();
@@ -745,16 +756,18 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
         }
       }
     }
+    if (!ROT) {
 #pragma unroll
-    for (int i = 0; i < 2 * R; ++i) {
-      qu[i] = qu[i + G::U];
-      qy[i] = qy[i + G::U];
-      qz[i] = qz[i + G::U];
-    }
+      for (int i = 0; i < 2 * R; ++i) {
+        qu[i] = qu[i + G::U];
+        qy[i] = qy[i + G::U];
+        qz[i] = qz[i + G::U];
+      }
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      gq[i] = gq[i + G::U];
-      pl[i] = pl[i + G::U];
+      for (int i = 0; i < R; ++i) {
+        gq[i] = gq[i + G::U];
+        pl[i] = pl[i + G::U];
+      }
     }
   }
 }
