@@ -74,7 +74,7 @@ def _acoustic_cfg(B, order, dims, steps=4):
 @pytest.mark.parametrize("variant,order,dims", [
     ("queue", 8, (40, 37, 45)), ("queue", 16, (36, 35, 41)), ("queue", 2, (20, 19, 23)),
     ("tma", 8, (40, 37, 45)), ("direct", 6, (20, 19, 23)), ("persistent", 4, (24, 21, 27)),
-    ("cluster", 4, (32, 30, 34))])
+    ("cluster", 4, (32, 30, 34)), ("tb2", 4, (40, 37, 45)), ("tb2", 8, (36, 35, 41))])
 def test_acoustic_canaries_and_determinism(B, variant, order, dims):
     import torch
 
@@ -119,7 +119,8 @@ def test_fp64_canaries(B):
     assert ar.intact() and fld.halo_is_zero()
 
 
-def test_tti_canaries_and_determinism(B):
+@pytest.mark.parametrize("interleaved", [True, False])
+def test_tti_canaries_and_determinism(B, interleaved):
     import torch
 
     from paper_1608_03984_b200 import tti
@@ -134,8 +135,14 @@ def test_tti_canaries_and_determinism(B):
                         source=B.Source((nx - 1, ny - 1, nz - 1), 1e3 * ricker(25.0, 1e-3, 4)))
     out = []
     for rep in range(3):
-        ar = Arena([(nx, ny, 32)] * 6 + [(cfg.n_t, nx)], torch.float32)
-        f = tti.TTIWavefield(cfg.halo, ar.views[:3], ar.views[3:6], dims)
+        if interleaved:  # (p, r) pairs per point, one array per level (ABI 4)
+            ar = Arena([(nx, ny, 32, 2)] * 3 + [(cfg.n_t, nx)], torch.float32)
+            f = tti.TTIWavefield(cfg.halo, [v[..., 0] for v in ar.views[:3]],
+                                 [v[..., 1] for v in ar.views[:3]], dims, interleaved=True)
+            ar.views = ar.views[:3] + [None, None, None] + ar.views[3:]
+        else:
+            ar = Arena([(nx, ny, 32)] * 6 + [(cfg.n_t, nx)], torch.float32)
+            f = tti.TTIWavefield(cfg.halo, ar.views[:3], ar.views[3:6], dims)
         f.traces = ar.views[6]
         tti.tti_run(f, cfg)
         torch.cuda.synchronize()
