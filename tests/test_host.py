@@ -206,3 +206,52 @@ def test_oracle_cache_keys_and_reuse(tmp_path, monkeypatch):
     assert np.array_equal(cache.cached(k1, compute)["a"], np.arange(4.0))
     assert np.array_equal(cache.cached(k1, compute)["a"], np.arange(4.0))
     assert len(calls) == 1
+
+
+def test_tti_interleaved_layout_validated_without_gpu():
+    """ABI 4's fdr_tti_args.interleaved: r[i] must be p[i] + 1 float, the flag
+    0 or 1, and the TMA (tti_stream) variant takes separate levels only."""
+    from paper_1608_03984_b200 import tti
+
+    lib = _lib.load()
+    assert lib.fdr_tti_args_size() == ctypes.sizeof(tti._TTIArgs)
+    a = tti._TTIArgs()
+    a.abi_version = _lib.ABI_VERSION
+    a.order = 8
+    a.nx = a.ny = a.nz = 24
+    a.pitch_y, a.pitch_x = 24, 24 * 24
+    base = 1 << 20  # fake device addresses: validation runs before any CUDA call
+    for i in range(3):
+        a.p[i] = base + i * 4096
+        a.r[i] = base + i * 4096 + 4
+    for i in range(9):
+        a.params[i] = base + 65536 + i * 4096
+    a.n_steps = 1
+    a.interleaved = 1
+    a.r[2] = base + 2 * 4096 + 8  # not p + 1 float
+    with pytest.raises(B.ValidationError, match="r\\[i\\] == p\\[i\\] \\+ 1"):
+        _lib.check(lib.fdr_tti_run(ctypes.byref(a), None))
+    a.r[2] = base + 2 * 4096 + 4
+    a.interleaved = 2
+    with pytest.raises(B.ValidationError, match="interleaved must be 0 or 1"):
+        _lib.check(lib.fdr_tti_run(ctypes.byref(a), None))
+    a.interleaved = 1
+    a.variant = _lib.VARIANT_TMA
+    with pytest.raises(B.ValidationError, match="separate p/r levels"):
+        _lib.check(lib.fdr_tti_run(ctypes.byref(a), None))
+
+
+def test_tb2_variant_is_known_to_the_library():
+    args = _lib.AcousticArgs()
+    args.abi_version = _lib.ABI_VERSION
+    args.order = 8
+    args.nx = args.ny = args.nz = 5  # rejected for its size, not for the variant
+    args.pitch_y, args.pitch_x = 8, 40
+    args.variant = _lib.VARIANT_TB2
+    with pytest.raises(B.ValidationError, match="too small"):
+        _lib.check(_lib.load().fdr_acoustic_run(ctypes.byref(args), None))
+    args.nx = args.ny = args.nz = 16
+    args.pitch_y, args.pitch_x = 16, 256
+    args.variant = _lib.VARIANT_TB2 + 1
+    with pytest.raises(B.ValidationError, match="unknown variant"):
+        _lib.check(_lib.load().fdr_acoustic_run(ctypes.byref(args), None))
