@@ -46,8 +46,8 @@ def test_f32_oracle_accuracy_vs_f64(order):
     f64, tr64 = E.simulate_f64(cfg)
     assert np.abs(f64["vz"]).max() > 1e-6
     for k in FIELDS:
-        assert rel_l2(st.interior(k), f64[k]) < 2e-5, k
-    assert rel_l2(st.traces, tr64) < 2e-5
+        assert rel_l2(st.interior(k), f64[k]) < 1e-5, k  # north_star tolerance (measured <= 2.4e-7)
+    assert rel_l2(st.traces, tr64) < 1e-5
 
 
 def test_c_oracle_threads_bitexact():

@@ -78,9 +78,9 @@ def test_f32_oracle_accuracy_vs_f64(order):
     p64, r64, tr64 = T.simulate_f64(cfg)
     assert np.isfinite(st.interior()).all()
     assert np.abs(p64).max() > 1e-3  # the wavefield is non-trivial
-    assert rel_l2(st.interior("p"), p64) < 2e-5
-    assert rel_l2(st.interior("r"), r64) < 2e-5
-    assert rel_l2(st.traces, tr64) < 2e-5
+    assert rel_l2(st.interior("p"), p64) < 1e-5  # north_star tolerance (measured 3e-7 .. 5e-7)
+    assert rel_l2(st.interior("r"), r64) < 1e-5
+    assert rel_l2(st.traces, tr64) < 1e-5
 
 
 def test_c_oracle_threads_bitexact():
