@@ -142,6 +142,10 @@ EXPORTS = (
     ("fdr_tti_run", ctypes.c_int, (ctypes.c_void_p, _vp)),
     ("fdr_elastic_args_size", ctypes.c_size_t, ()),
     ("fdr_elastic_run", ctypes.c_int, (ctypes.c_void_p, _vp)),
+    ("fdr_tti64_args_size", ctypes.c_size_t, ()),
+    ("fdr_tti64_run", ctypes.c_int, (ctypes.c_void_p, _vp)),
+    ("fdr_elastic64_args_size", ctypes.c_size_t, ()),
+    ("fdr_elastic64_run", ctypes.c_int, (ctypes.c_void_p, _vp)),
     ("fdr_acoustic64_args_size", ctypes.c_size_t, ()),
     ("fdr_acoustic64_run", ctypes.c_int, (ctypes.POINTER(Acoustic64Args), _vp)),
     ("fdr_selftest_division64", ctypes.c_int64,

@@ -1038,6 +1038,181 @@ int el_stream_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, 
   }
 }
 
+
+// ========================================================= float64 path
+// fdr_elastic64_run: el_vel_direct / el_str_direct (= oracle/elastic_ref.c)
+// in IEEE double: the float64 reference of the float32 path's error.
+struct ElStep64 {
+  double* f[9];
+  const double *bs, *lam, *mu;
+  int nx, ny, nz, pitch_y;
+  long long pitch_x;
+  int radius;
+  double c[FDR_MAX_RADIUS + 1];
+  const double *gx, *gy, *gz, *series;
+  int n_series, it, sx, sy, sz;
+  const int* rec;
+  int n_rec;
+  double* traces;
+  int gather_row;
+};
+
+__device__ __forceinline__ double at64(const double* u, const ElStep64& a, int x, int y, int z) {
+  if (x < 0 || x >= a.nx || y < 0 || y >= a.ny || z < 0 || z >= a.nz) return 0.0;
+  return u[(size_t)x * a.pitch_x + (size_t)y * a.pitch_y + z];
+}
+__device__ double dF64(const double* u, const ElStep64& a, int x, int y, int z, int ax) {
+  const int dx = ax == 0, dy = ax == 1, dz = ax == 2;
+  double d = __dmul_rn(a.c[1], __dsub_rn(at64(u, a, x + dx, y + dy, z + dz), at64(u, a, x, y, z)));
+  for (int k = 2; k <= a.radius; ++k)
+    d = __fma_rn(a.c[k], __dsub_rn(at64(u, a, x + k * dx, y + k * dy, z + k * dz),
+                                   at64(u, a, x + (1 - k) * dx, y + (1 - k) * dy, z + (1 - k) * dz)), d);
+  return d;
+}
+__device__ double dB64(const double* u, const ElStep64& a, int x, int y, int z, int ax) {
+  const int dx = ax == 0, dy = ax == 1, dz = ax == 2;
+  double d = __dmul_rn(a.c[1], __dsub_rn(at64(u, a, x, y, z), at64(u, a, x - dx, y - dy, z - dz)));
+  for (int k = 2; k <= a.radius; ++k)
+    d = __fma_rn(a.c[k], __dsub_rn(at64(u, a, x + (k - 1) * dx, y + (k - 1) * dy, z + (k - 1) * dz),
+                                   at64(u, a, x - k * dx, y - k * dy, z - k * dz)), d);
+  return d;
+}
+__device__ __forceinline__ double taper64(const ElStep64& a, int x, int y, int z) {
+  return __dmul_rn(__dmul_rn(a.gx[x], a.gy[y]), a.gz[z]);
+}
+
+__global__ void __launch_bounds__(256) el_vel_direct64(const ElStep64 a) {
+  const int z = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int x = blockIdx.z;
+  if (z >= a.nz || y >= a.ny) return;
+  const size_t o = (size_t)x * a.pitch_x + (size_t)y * a.pitch_y + z;
+  const double b = a.bs[o];
+  const double ax = __dadd_rn(__dadd_rn(dB64(a.f[SXY], a, x, y, z, 1), dB64(a.f[SXZ], a, x, y, z, 2)),
+                              dF64(a.f[SXX], a, x, y, z, 0));
+  const double ay = __dadd_rn(__dadd_rn(dF64(a.f[SYY], a, x, y, z, 1), dB64(a.f[SYZ], a, x, y, z, 2)),
+                              dB64(a.f[SXY], a, x, y, z, 0));
+  const double az = __dadd_rn(__dadd_rn(dB64(a.f[SYZ], a, x, y, z, 1), dF64(a.f[SZZ], a, x, y, z, 2)),
+                              dB64(a.f[SXZ], a, x, y, z, 0));
+  double vx = __fma_rn(b, ax, a.f[VX][o]), vy = __fma_rn(b, ay, a.f[VY][o]);
+  double vz = __fma_rn(b, az, a.f[VZ][o]);
+  if (a.gx) {
+    const double g = taper64(a, x, y, z);
+    vx = __dmul_rn(vx, g);
+    vy = __dmul_rn(vy, g);
+    vz = __dmul_rn(vz, g);
+  }
+  a.f[VX][o] = vx;
+  a.f[VY][o] = vy;
+  a.f[VZ][o] = vz;
+}
+
+__global__ void __launch_bounds__(256) el_str_direct64(const ElStep64 a) {
+  if (a.gather_row >= 0) {  // vz is final for this step and not written here
+    const int nthr = blockDim.x * blockDim.y;
+    const int bi = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int t = threadIdx.x + blockDim.x * threadIdx.y;
+    for (int i = bi * nthr + t; i < a.n_rec; i += nthr * (int)(gridDim.x * gridDim.y * gridDim.z)) {
+      const int* q = a.rec + 3 * i;
+      a.traces[(size_t)a.gather_row * a.n_rec + i] =
+          a.f[VZ][(size_t)q[0] * a.pitch_x + (size_t)q[1] * a.pitch_y + q[2]];
+    }
+  }
+  const int z = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int x = blockIdx.z;
+  if (z >= a.nz || y >= a.ny) return;
+  const size_t o = (size_t)x * a.pitch_x + (size_t)y * a.pitch_y + z;
+  const double lam = a.lam[o], mu = a.mu[o];
+  const double l2m = __fma_rn(2.0, mu, lam);
+  const double ex = dB64(a.f[VX], a, x, y, z, 0), ey = dB64(a.f[VY], a, x, y, z, 1);
+  const double ez = dB64(a.f[VZ], a, x, y, z, 2);
+  double s[6];
+  s[0] = __fma_rn(lam, __dadd_rn(ey, ez), __fma_rn(l2m, ex, a.f[SXX][o]));
+  s[1] = __fma_rn(lam, __dadd_rn(ez, ex), __fma_rn(l2m, ey, a.f[SYY][o]));
+  s[2] = __fma_rn(lam, __dadd_rn(ey, ex), __fma_rn(l2m, ez, a.f[SZZ][o]));
+  s[3] = __fma_rn(mu, __dadd_rn(dF64(a.f[VX], a, x, y, z, 1), dF64(a.f[VY], a, x, y, z, 0)), a.f[SXY][o]);
+  s[4] = __fma_rn(mu, __dadd_rn(dF64(a.f[VX], a, x, y, z, 2), dF64(a.f[VZ], a, x, y, z, 0)), a.f[SXZ][o]);
+  s[5] = __fma_rn(mu, __dadd_rn(dF64(a.f[VY], a, x, y, z, 2), dF64(a.f[VZ], a, x, y, z, 1)), a.f[SYZ][o]);
+  if (a.gx) {
+    const double g = taper64(a, x, y, z);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) s[i] = __dmul_rn(s[i], g);
+  }
+  if (x == a.sx && y == a.sy && z == a.sz && a.it < a.n_series) {
+    const double q = a.series[a.it];
+    s[0] = __dadd_rn(s[0], q);
+    s[1] = __dadd_rn(s[1], q);
+    s[2] = __dadd_rn(s[2], q);
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) a.f[SXX + i][o] = s[i];
+}
+
+static int validate64(const fdr_elastic64_args* a) {
+  if (!a) return fail(FDR_EINVAL, "args is NULL");
+  if (a->abi_version != FDR_ABI_VERSION)
+    return fail(FDR_EINVAL, "abi_version %d != library %d", a->abi_version, FDR_ABI_VERSION);
+  if (a->order < 2 || a->order % 2 || a->order > 16)
+    return fail(FDR_EINVAL, "elastic order must be even and within [2, 16], got %d", a->order);
+  const int r = a->order / 2;
+  if (a->nx < 2 * r + 1 || a->ny < 2 * r + 1 || a->nz < 2 * r + 1)
+    return fail(FDR_EINVAL, "interior dims (%d, %d, %d) too small for halo width %d", a->nx,
+                a->ny, a->nz, r);
+  if (a->pitch_y < a->nz || a->pitch_x < (int64_t)a->ny * a->pitch_y)
+    return fail(FDR_EINVAL, "bad pitches");
+  if (a->n_steps < 0 || a->it0 < 0) return fail(FDR_EINVAL, "n_steps and it0 must be >= 0");
+  for (int i = 0; i < 9; ++i)
+    if (!a->fields[i]) return fail(FDR_EINVAL, "field %d is NULL", i);
+  for (int i = 0; i < 3; ++i)
+    if (!a->params[i]) return fail(FDR_EINVAL, "parameter grid %d is NULL", i);
+  if (a->sponge_x && (!a->sponge_y || !a->sponge_z))
+    return fail(FDR_EINVAL, "sponge needs all three profiles");
+  if (a->src_x >= 0 && (a->src_x >= a->nx || a->src_y < 0 || a->src_y >= a->ny ||
+                        a->src_z < 0 || a->src_z >= a->nz))
+    return fail(FDR_EINVAL, "source location outside interior");
+  if (a->n_rec > 0 && (!a->rec_xyz || !a->traces))
+    return fail(FDR_EINVAL, "receiver coordinates or trace buffer NULL");
+  return FDR_OK;
+}
+
+static int run64(const fdr_elastic64_args* a, cudaStream_t st) {
+  for (int k = 0; k < a->n_steps; ++k) {
+    ElStep64 s;
+    memset(&s, 0, sizeof(s));
+    for (int i = 0; i < 9; ++i) s.f[i] = a->fields[i];
+    s.bs = a->params[0];
+    s.lam = a->params[1];
+    s.mu = a->params[2];
+    s.nx = a->nx;
+    s.ny = a->ny;
+    s.nz = a->nz;
+    s.pitch_y = a->pitch_y;
+    s.pitch_x = a->pitch_x;
+    s.radius = a->order / 2;
+    for (int j = 0; j <= FDR_MAX_RADIUS; ++j) s.c[j] = a->c[j];
+    s.gx = a->sponge_x;
+    s.gy = a->sponge_y;
+    s.gz = a->sponge_z;
+    s.series = a->series;
+    s.n_series = (a->src_x >= 0 && a->series) ? a->n_series : 0;
+    s.it = a->it0 + k;
+    s.sx = a->src_x;
+    s.sy = a->src_y;
+    s.sz = a->src_z;
+    s.rec = a->rec_xyz;
+    s.n_rec = a->n_rec;
+    s.traces = a->traces;
+    s.gather_row = (a->n_rec > 0 && a->traces && s.it < a->trace_rows) ? s.it : -1;
+    dim3 block(64, 4, 1), grid((a->nz + 63) / 64, (a->ny + 3) / 4, a->nx);
+    el_vel_direct64<<<grid, block, 0, st>>>(s);
+    EL_CUDA(cudaGetLastError());
+    el_str_direct64<<<grid, block, 0, st>>>(s);
+    EL_CUDA(cudaGetLastError());
+  }
+  return FDR_OK;
+}
+
 }  // namespace fdr_el
 
 extern "C" {
@@ -1048,6 +1223,14 @@ int fdr_elastic_run(const fdr_elastic_args* args, void* stream) {
   int rc = fdr_el::validate(args);
   if (rc != FDR_OK) return rc;
   return fdr_el::run(args, static_cast<cudaStream_t>(stream));
+}
+
+size_t fdr_elastic64_args_size(void) { return sizeof(fdr_elastic64_args); }
+
+int fdr_elastic64_run(const fdr_elastic64_args* args, void* stream) {
+  int rc = fdr_el::validate64(args);
+  if (rc != FDR_OK) return rc;
+  return fdr_el::run64(args, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

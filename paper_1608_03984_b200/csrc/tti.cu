@@ -968,6 +968,191 @@ static int run(const fdr_tti_args* a, cudaStream_t st) {
   return (2 + a->n_steps) % 3;
 }
 
+
+// ========================================================= float64 path
+// fdr_tti64_run: the direct kernel's per-point sequence (= oracle/tti_ref.c)
+// with every value in IEEE double, on separate p and r levels.  The float64
+// reference the float32 path's error is reported against (SURVEY.md §8(f)3
+// for TTI; precision_bytes = 8, equations.py:74-78).
+struct TTIStep64 {
+  const double *p, *pp, *r, *rp;
+  double *pn, *rn;
+  const double* prm[9];
+  int nx, ny, nz, pitch_y;
+  long long pitch_x;
+  int radius;
+  double w2[FDR_MAX_RADIUS + 1];
+  double w1[FDR_MAX_RADIUS + 1];
+  const double *gx, *gy, *gz, *series;
+  int n_series, it, sx, sy, sz;
+  const int* rec;
+  int n_rec;
+  double* traces;
+  int gather_row;
+};
+
+__device__ __forceinline__ double at64(const double* u, const TTIStep64& a, int x, int y, int z) {
+  if (x < 0 || x >= a.nx || y < 0 || y >= a.ny || z < 0 || z >= a.nz) return 0.0;
+  return u[(size_t)x * a.pitch_x + (size_t)y * a.pitch_y + z];
+}
+__device__ double d1_64(const double* u, const TTIStep64& a, int x, int y, int z, int ax) {
+  const int dx = ax == 0, dy = ax == 1, dz = ax == 2;
+  double d = __dmul_rn(a.w1[1], __dsub_rn(at64(u, a, x + dx, y + dy, z + dz), at64(u, a, x - dx, y - dy, z - dz)));
+  for (int j = 2; j <= a.radius; ++j)
+    d = __fma_rn(a.w1[j], __dsub_rn(at64(u, a, x + j * dx, y + j * dy, z + j * dz),
+                                    at64(u, a, x - j * dx, y - j * dy, z - j * dz)), d);
+  return d;
+}
+__device__ double d2_64(const double* u, const TTIStep64& a, int x, int y, int z, int ax) {
+  const int dx = ax == 0, dy = ax == 1, dz = ax == 2;
+  double d = __dmul_rn(a.w2[0], at64(u, a, x, y, z));
+  for (int j = 1; j <= a.radius; ++j)
+    d = __fma_rn(a.w2[j], __dadd_rn(at64(u, a, x + j * dx, y + j * dy, z + j * dz),
+                                    at64(u, a, x - j * dx, y - j * dy, z - j * dz)), d);
+  return d;
+}
+__device__ double d11_64(const double* u, const TTIStep64& a, int x, int y, int z, int ao, int ai) {
+  const int dx = ao == 0, dy = ao == 1, dz = ao == 2;
+  double d = __dmul_rn(a.w1[1], __dsub_rn(d1_64(u, a, x + dx, y + dy, z + dz, ai),
+                                          d1_64(u, a, x - dx, y - dy, z - dz, ai)));
+  for (int j = 2; j <= a.radius; ++j)
+    d = __fma_rn(a.w1[j], __dsub_rn(d1_64(u, a, x + j * dx, y + j * dy, z + j * dz, ai),
+                                    d1_64(u, a, x - j * dx, y - j * dy, z - j * dz, ai)), d);
+  return d;
+}
+__device__ void gl_op64(const double* u, const TTIStep64& a, int x, int y, int z, const double* c,
+                        double* G, double* L) {
+  const double dxx = d2_64(u, a, x, y, z, 0), dyy = d2_64(u, a, x, y, z, 1), dzz = d2_64(u, a, x, y, z, 2);
+  const double dxy = d11_64(u, a, x, y, z, 0, 1), dxz = d11_64(u, a, x, y, z, 0, 2);
+  const double dyz = d11_64(u, a, x, y, z, 1, 2);
+  const double gin = __fma_rn(c[4], dyz, __fma_rn(c[2], dzz, __dmul_rn(c[1], dyy)));
+  const double lin = __dadd_rn(dyy, dzz);
+  *G = __fma_rn(c[5], dxz, __fma_rn(c[3], dxy, __fma_rn(c[0], dxx, gin)));
+  *L = __dadd_rn(lin, dxx);
+}
+
+__global__ void __launch_bounds__(256) tti_direct64(const TTIStep64 a) {
+  if (a.gather_row >= 0) {  // the previous step's p (cur here, read-only) at the receivers
+    const int nthr = blockDim.x * blockDim.y;
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int t = threadIdx.x + blockDim.x * threadIdx.y;
+    for (int i = b * nthr + t; i < a.n_rec; i += nthr * (int)(gridDim.x * gridDim.y * gridDim.z)) {
+      const int* c = a.rec + 3 * i;
+      a.traces[(size_t)a.gather_row * a.n_rec + i] =
+          a.p[(size_t)c[0] * a.pitch_x + (size_t)c[1] * a.pitch_y + c[2]];
+    }
+  }
+  const int z = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int x = blockIdx.z;
+  if (z >= a.nz || y >= a.ny) return;
+  const size_t o = (size_t)x * a.pitch_x + (size_t)y * a.pitch_y + z;
+  const double k = a.prm[0][o], pa = a.prm[1][o], pb = a.prm[2][o];
+  const double c[6] = {a.prm[3][o], a.prm[4][o], a.prm[5][o], a.prm[6][o], a.prm[7][o], a.prm[8][o]};
+  double Gp, Lp, Gr, Lr;
+  gl_op64(a.p, a, x, y, z, c, &Gp, &Lp);
+  gl_op64(a.r, a, x, y, z, c, &Gr, &Lr);
+  const double Hp = __dsub_rn(Lp, Gp);
+  double pn = __fma_rn(k, __fma_rn(pa, Hp, __dmul_rn(pb, Gr)), __fma_rn(2.0, a.p[o], -a.pp[o]));
+  double rn = __fma_rn(k, __fma_rn(pb, Hp, Gr), __fma_rn(2.0, a.r[o], -a.rp[o]));
+  if (a.gx) {
+    const double g = __dmul_rn(__dmul_rn(a.gx[x], a.gy[y]), a.gz[z]);
+    pn = __dmul_rn(pn, g);
+    rn = __dmul_rn(rn, g);
+  }
+  if (x == a.sx && y == a.sy && z == a.sz && a.it < a.n_series) {
+    pn = __dadd_rn(pn, a.series[a.it]);
+    rn = __dadd_rn(rn, a.series[a.it]);
+  }
+  a.pn[o] = pn;
+  a.rn[o] = rn;
+}
+
+__global__ void tti_gather64(const double* p, const int* rec, int n_rec, double* traces, int row,
+                             int pitch_y, long long pitch_x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_rec) {
+    const int* c = rec + 3 * i;
+    traces[(size_t)row * n_rec + i] = p[(size_t)c[0] * pitch_x + (size_t)c[1] * pitch_y + c[2]];
+  }
+}
+
+static int validate64(const fdr_tti64_args* a) {
+  if (!a) return fail(FDR_EINVAL, "args is NULL");
+  if (a->abi_version != FDR_ABI_VERSION)
+    return fail(FDR_EINVAL, "abi_version %d != library %d", a->abi_version, FDR_ABI_VERSION);
+  if (a->order < 2 || a->order % 2 || a->order > 16)
+    return fail(FDR_EINVAL, "TTI order must be even and within [2, 16], got %d", a->order);
+  const int r = a->order / 2;
+  if (a->nx < 2 * r + 1 || a->ny < 2 * r + 1 || a->nz < 2 * r + 1)
+    return fail(FDR_EINVAL, "interior dims (%d, %d, %d) too small for halo width %d", a->nx,
+                a->ny, a->nz, r);
+  if (a->pitch_y < a->nz || a->pitch_x < (int64_t)a->ny * a->pitch_y)
+    return fail(FDR_EINVAL, "bad pitches");
+  if (a->n_steps < 0 || a->it0 < 0) return fail(FDR_EINVAL, "n_steps and it0 must be >= 0");
+  for (int i = 0; i < 3; ++i)
+    if (!a->p[i] || !a->r[i]) return fail(FDR_EINVAL, "level pointer NULL");
+  for (int i = 0; i < 9; ++i)
+    if (!a->params[i]) return fail(FDR_EINVAL, "parameter grid %d is NULL", i);
+  if (a->sponge_x && (!a->sponge_y || !a->sponge_z))
+    return fail(FDR_EINVAL, "sponge needs all three profiles");
+  if (a->src_x >= 0 && (a->src_x >= a->nx || a->src_y < 0 || a->src_y >= a->ny ||
+                        a->src_z < 0 || a->src_z >= a->nz))
+    return fail(FDR_EINVAL, "source location outside interior");
+  if (a->n_rec > 0 && (!a->rec_xyz || !a->traces))
+    return fail(FDR_EINVAL, "receiver coordinates or trace buffer NULL");
+  return FDR_OK;
+}
+
+static int run64(const fdr_tti64_args* a, cudaStream_t st) {
+  for (int k = 0; k < a->n_steps; ++k) {
+    TTIStep64 s;
+    memset(&s, 0, sizeof(s));
+    s.pn = a->p[k % 3];
+    s.pp = a->p[(1 + k) % 3];
+    s.p = a->p[(2 + k) % 3];
+    s.rn = a->r[k % 3];
+    s.rp = a->r[(1 + k) % 3];
+    s.r = a->r[(2 + k) % 3];
+    for (int i = 0; i < 9; ++i) s.prm[i] = a->params[i];
+    s.nx = a->nx;
+    s.ny = a->ny;
+    s.nz = a->nz;
+    s.pitch_y = a->pitch_y;
+    s.pitch_x = a->pitch_x;
+    s.radius = a->order / 2;
+    for (int j = 0; j <= FDR_MAX_RADIUS; ++j) {
+      s.w2[j] = a->w2[j];
+      s.w1[j] = a->w1[j];
+    }
+    s.gx = a->sponge_x;
+    s.gy = a->sponge_y;
+    s.gz = a->sponge_z;
+    s.series = a->series;
+    s.n_series = (a->src_x >= 0 && a->series) ? a->n_series : 0;
+    s.it = a->it0 + k;
+    s.sx = a->src_x;
+    s.sy = a->src_y;
+    s.sz = a->src_z;
+    s.rec = a->rec_xyz;
+    s.n_rec = a->n_rec;
+    s.traces = a->traces;
+    const int row = s.it - 1;
+    s.gather_row = (k > 0 && a->n_rec > 0 && a->traces && row < a->trace_rows) ? row : -1;
+    dim3 block(64, 4, 1), grid((a->nz + 63) / 64, (a->ny + 3) / 4, a->nx);
+    tti_direct64<<<grid, block, 0, st>>>(s);
+    TTI_CUDA(cudaGetLastError());
+  }
+  const int last = a->it0 + a->n_steps - 1;
+  if (a->n_steps > 0 && a->n_rec > 0 && a->traces && last < a->trace_rows) {
+    tti_gather64<<<(a->n_rec + 255) / 256, 256, 0, st>>>(a->p[(2 + a->n_steps) % 3], a->rec_xyz,
+                                                        a->n_rec, a->traces, last, a->pitch_y,
+                                                        a->pitch_x);
+    TTI_CUDA(cudaGetLastError());
+  }
+  return (2 + a->n_steps) % 3;
+}
+
 }  // namespace fdr_tti
 
 extern "C" {
@@ -978,6 +1163,14 @@ int fdr_tti_run(const fdr_tti_args* args, void* stream) {
   int rc = fdr_tti::validate(args);
   if (rc != FDR_OK) return rc;
   return fdr_tti::run(args, static_cast<cudaStream_t>(stream));
+}
+
+size_t fdr_tti64_args_size(void) { return sizeof(fdr_tti64_args); }
+
+int fdr_tti64_run(const fdr_tti64_args* args, void* stream) {
+  int rc = fdr_tti::validate64(args);
+  if (rc != FDR_OK) return rc;
+  return fdr_tti::run64(args, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

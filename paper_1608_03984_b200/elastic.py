@@ -46,6 +46,12 @@ def elastic_weights_f32(order: int) -> np.ndarray:
     return np.array([0.0] + [float(v) for v in c], dtype=np.float32)
 
 
+def elastic_weights_f64(order: int) -> np.ndarray:
+    """c[0..r] float64 of the exact rationals (the float64 path)."""
+    c = staggered_first_derivative_weights(order)
+    return np.array([0.0] + [float(v) for v in c], dtype=np.float64)
+
+
 def elastic_max_stable_dt(order: int, h: float, vp_max: float) -> float:
     """Staggered leapfrog bound dt <= h / (sqrt(3) vp_max sum|c_k|)."""
     s = float(sum(abs(v) for v in staggered_first_derivative_weights(order)))
@@ -102,7 +108,9 @@ class ElasticConfig:
     def halo(self) -> int:
         return self.order // 2
 
-    def params(self) -> dict:
+    def params(self, precision: int = 4) -> dict:
+        """bs, lam, mu computed in float64; rounded once to float32 unless
+        precision == 8 (the float64 path, fdr_elastic64_run)."""
         shape = tuple(self.dims)
 
         def grid(v):
@@ -113,7 +121,8 @@ class ElasticConfig:
         lam = rho * vp * vp - 2.0 * mu
         f = self.dt / self.h
         out = {"bs": f / rho, "lam": f * lam, "mu": f * mu}
-        return {k: np.ascontiguousarray(v, dtype=np.float32) for k, v in out.items()}
+        dt = np.float64 if precision == 8 else np.float32
+        return {k: np.ascontiguousarray(v, dtype=dt) for k, v in out.items()}
 
 
 def _torch():
@@ -133,13 +142,18 @@ class ElasticWavefield:
         self.traces = None
 
     @classmethod
-    def allocate(cls, dims, halo, device=None):
+    def allocate(cls, dims, halo, device=None, dtype=None):
+        """float32 fields (default), or dtype=torch.float64 for the float64
+        path (fdr_elastic64_run, the direct kernel in double)."""
         torch = _torch()
         _lib.load()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        dtype = torch.float32 if dtype is None else dtype
+        if dtype not in (torch.float32, torch.float64):
+            raise ValidationError("elastic fields are float32 or float64")
         nx, ny, nz = (int(d) for d in dims)
         shape = (nx, ny, row_pitch(nz))
-        return cls(halo, [torch.zeros(shape, dtype=torch.float32, device=dev) for _ in FIELDS],
+        return cls(halo, [torch.zeros(shape, dtype=dtype, device=dev) for _ in FIELDS],
                    (nx, ny, nz))
 
     @property
@@ -161,7 +175,8 @@ class ElasticWavefield:
 
     def set_interior(self, name: str, values) -> None:
         torch = _torch()
-        arr = np.ascontiguousarray(np.asarray(values, dtype=np.float32))
+        f64 = self.fields[0].dtype == torch.float64
+        arr = np.ascontiguousarray(np.asarray(values, dtype=np.float64 if f64 else np.float32))
         if arr.shape != self._dims:
             raise ValidationError("interior values do not match dims")
         self.fields[FIELDS.index(name)][:, :, : self._dims[2]].copy_(host_tensor(arr))
@@ -185,23 +200,49 @@ class _ElArgs(ctypes.Structure):
     ]
 
 
+class _ElArgs64(ctypes.Structure):
+    """Mirror of fdr_elastic64_args (include/b200fd.h)."""
+
+    _fields_ = [
+        ("abi_version", ctypes.c_int32), ("order", ctypes.c_int32),
+        ("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+        ("pitch_y", ctypes.c_int32), ("pitch_x", ctypes.c_int64),
+        ("c", ctypes.c_double * (_lib.MAX_RADIUS + 1)),
+        ("params", ctypes.c_void_p * 3), ("fields", ctypes.c_void_p * 9),
+        ("sponge_x", ctypes.c_void_p), ("sponge_y", ctypes.c_void_p), ("sponge_z", ctypes.c_void_p),
+        ("series", ctypes.c_void_p), ("n_series", ctypes.c_int32),
+        ("src_x", ctypes.c_int32), ("src_y", ctypes.c_int32), ("src_z", ctypes.c_int32),
+        ("n_rec", ctypes.c_int32), ("rec_xyz", ctypes.c_void_p), ("traces", ctypes.c_void_p),
+        ("trace_rows", ctypes.c_int32), ("it0", ctypes.c_int32), ("n_steps", ctypes.c_int32),
+    ]
+
+
 class _ElPlan:
-    def __init__(self, cfg: ElasticConfig, device, pitch: int):
+    """Device copies of a config's inputs; precision 8: everything in double
+    (parameters unrounded, exact float64 weights, float64 sponge and series)."""
+
+    def __init__(self, cfg: ElasticConfig, device, pitch: int, precision: int = 4):
         torch = _torch()
         self.key = _el_key(cfg, device, pitch)
         self.guard = InputGuard(config_inputs(cfg, _EL_FIELDS))  # frozen while cached
         nx, ny, nz = cfg.dims
-        self.c = elastic_weights_f32(cfg.order)
+        f64 = precision == 8
+        tdt, ndt = (torch.float64, np.float64) if f64 else (torch.float32, np.float32)
+        self.c = elastic_weights_f64(cfg.order) if f64 else elastic_weights_f32(cfg.order)
         self.params = []
-        for host in cfg.params().values():
-            t = torch.zeros((nx, ny, pitch), dtype=torch.float32, device=device)
+        for host in cfg.params(precision).values():
+            t = torch.zeros((nx, ny, pitch), dtype=tdt, device=device)
             t[:, :, :nz].copy_(host_tensor(host))
             self.params.append(t)
         self.sponge = None if cfg.sponge is None else tuple(
-            host_tensor(v).to(device) for v in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
+            host_tensor(np.asarray(v, dtype=ndt)).to(device)
+            for v in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
         self.series, self.src, self.n_series = None, (-1, 0, 0), 0
         if cfg.source is not None:
-            s = np.ascontiguousarray(np.asarray(cfg.source.series).astype(np.float32).reshape(-1))
+            # float32 samples (what the float32 path injects), converted exactly
+            # to double on the float64 path, as the acoustic float64 path does
+            s = np.ascontiguousarray(np.asarray(cfg.source.series).astype(np.float32)
+                                     .astype(ndt).reshape(-1))
             self.series = host_tensor(s).to(device)
             self.src = tuple(int(v) for v in cfg.source.location)
             self.n_series = int(s.size)
@@ -239,9 +280,13 @@ def elastic_run(fld: ElasticWavefield, cfg: ElasticConfig, n_steps: Optional[int
     lib = _lib.load()
     dev = fld.device
     pitch_y = int(fld.fields[0].shape[2])
-    plan = cached_plan(cfg, "_device_plan", _el_key(cfg, dev, pitch_y),
-                       lambda: _ElPlan(cfg, dev, pitch_y))
-    a = _ElArgs()
+    f64 = fld.fields[0].dtype == torch.float64
+    if f64 and variant not in ("auto", "direct"):
+        raise ValidationError("the float64 elastic path is the direct kernel (variant auto or direct)")
+    prec = 8 if f64 else 4
+    plan = cached_plan(cfg, "_device_plan64" if f64 else "_device_plan", _el_key(cfg, dev, pitch_y),
+                       lambda: _ElPlan(cfg, dev, pitch_y, prec))
+    a = _ElArgs64() if f64 else _ElArgs()
     a.abi_version = _lib.ABI_VERSION
     a.order = cfg.order
     a.nx, a.ny, a.nz = fld.dims
@@ -262,18 +307,23 @@ def elastic_run(fld: ElasticWavefield, cfg: ElasticConfig, n_steps: Optional[int
     if plan.rec is not None:
         rows = max(cfg.n_t, fld.it + n)
         n_rec = cfg.receivers.count
-        if fld.traces is None or fld.traces.shape[0] < rows or fld.traces.shape[1] != n_rec:
-            fld.traces = grow_traces(fld, rows, n_rec, torch.float32, dev)
+        tdt = torch.float64 if f64 else torch.float32
+        if (fld.traces is None or fld.traces.shape[0] < rows or fld.traces.shape[1] != n_rec
+                or fld.traces.dtype != tdt):
+            fld.traces = grow_traces(fld, rows, n_rec, tdt, dev)
         a.n_rec = n_rec
         a.rec_xyz = plan.rec.data_ptr()
         a.traces = fld.traces.data_ptr()
         a.trace_rows = int(fld.traces.shape[0])
     a.it0 = fld.it
     a.n_steps = n
-    a.variant = _VARIANTS[variant]
     stream = torch.cuda.current_stream(dev).cuda_stream
     with torch.cuda.device(dev):
-        _lib.check(lib.fdr_elastic_run(ctypes.byref(a), ctypes.c_void_p(stream)))
+        if f64:
+            _lib.check(lib.fdr_elastic64_run(ctypes.byref(a), ctypes.c_void_p(stream)))
+        else:
+            a.variant = _VARIANTS[variant]
+            _lib.check(lib.fdr_elastic_run(ctypes.byref(a), ctypes.c_void_p(stream)))
     fld.it += n
     return fld
 

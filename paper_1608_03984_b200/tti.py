@@ -54,6 +54,16 @@ def tti_weights_f32(order: int):
     return a2, a1
 
 
+def tti_weights_f64(order: int):
+    """(w2[0..r], w1[0..r]) float64 of the exact rationals (the float64 path)."""
+    r = order // 2
+    w2 = second_derivative_weights(order)
+    w1 = first_derivative_weights(order)
+    a2 = np.array([float(w2[r])] + [float(w2[r + j]) for j in range(1, r + 1)], dtype=np.float64)
+    a1 = np.array([0.0] + [float(w1[r + j]) for j in range(1, r + 1)], dtype=np.float64)
+    return a2, a1
+
+
 def tti_max_stable_dt(order: int, h: float, m, epsilon) -> float:
     """CFL-style bound h*sqrt(4/a2)/(v_max*sqrt(1+2 eps_max)) (cf. kernel.py:35-46)."""
     a2 = 3.0 * float(sum(abs(w) for w in second_derivative_weights(order)))
@@ -116,8 +126,9 @@ class TTIConfig:
     def halo(self) -> int:
         return self.order // 2
 
-    def params(self) -> dict:
-        """The 9 float32 parameter grids (host, float64 then rounded once)."""
+    def params(self, precision: int = 4) -> dict:
+        """The 9 parameter grids (host, float64; rounded once to float32 unless
+        precision == 8, the float64 path)."""
         shape = tuple(self.dims)
 
         def grid(v):
@@ -138,7 +149,8 @@ class TTIConfig:
             "cyz": sp * np.sin(2.0 * th),
             "cxz": cp * np.sin(2.0 * th),
         }
-        return {k: np.ascontiguousarray(v, dtype=np.float32) for k, v in out.items()}
+        dt = np.float64 if precision == 8 else np.float32
+        return {k: np.ascontiguousarray(v, dtype=dt) for k, v in out.items()}
 
 
 def _torch():
@@ -166,12 +178,19 @@ class TTIWavefield:
         self.interleaved = bool(interleaved)
 
     @classmethod
-    def allocate(cls, dims, halo, device=None, interleaved=True):
+    def allocate(cls, dims, halo, device=None, interleaved=True, dtype=None):
+        """dtype=torch.float64 allocates separate float64 levels for the
+        float64 path (fdr_tti64_run, the direct kernel in double)."""
         torch = _torch()
         _lib.load()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         nx, ny, nz = (int(d) for d in dims)
         shape = (nx, ny, row_pitch(nz))
+        if dtype is not None and dtype != torch.float32:
+            if dtype != torch.float64:
+                raise ValidationError("TTI levels are float32 or float64")
+            mk64 = lambda: [torch.zeros(shape, dtype=torch.float64, device=dev) for _ in range(3)]  # noqa: E731
+            return cls(halo, mk64(), mk64(), (nx, ny, nz))
         if interleaved:
             levels = [torch.zeros(shape + (2,), dtype=torch.float32, device=dev) for _ in range(3)]
             return cls(halo, [t[..., 0] for t in levels], [t[..., 1] for t in levels], (nx, ny, nz),
@@ -206,7 +225,8 @@ class TTIWavefield:
 
     def set_interior(self, field: str, level: int, values) -> None:
         torch = _torch()
-        arr = np.ascontiguousarray(np.asarray(values, dtype=np.float32))
+        f64 = self.p[0].dtype == torch.float64
+        arr = np.ascontiguousarray(np.asarray(values, dtype=np.float64 if f64 else np.float32))
         if arr.shape != self._dims:
             raise ValidationError("interior values do not match dims")
         (self.p if field == "p" else self.r)[level][:, :, : self._dims[2]].copy_(host_tensor(arr))
@@ -230,23 +250,49 @@ class _TTIArgs(ctypes.Structure):
     ]
 
 
+class _TTIArgs64(ctypes.Structure):
+    """Mirror of fdr_tti64_args (include/b200fd.h)."""
+
+    _fields_ = [
+        ("abi_version", ctypes.c_int32), ("order", ctypes.c_int32),
+        ("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+        ("pitch_y", ctypes.c_int32), ("pitch_x", ctypes.c_int64),
+        ("w2", ctypes.c_double * (_lib.MAX_RADIUS + 1)), ("w1", ctypes.c_double * (_lib.MAX_RADIUS + 1)),
+        ("params", ctypes.c_void_p * 9), ("p", ctypes.c_void_p * 3), ("r", ctypes.c_void_p * 3),
+        ("sponge_x", ctypes.c_void_p), ("sponge_y", ctypes.c_void_p), ("sponge_z", ctypes.c_void_p),
+        ("series", ctypes.c_void_p), ("n_series", ctypes.c_int32),
+        ("src_x", ctypes.c_int32), ("src_y", ctypes.c_int32), ("src_z", ctypes.c_int32),
+        ("n_rec", ctypes.c_int32), ("rec_xyz", ctypes.c_void_p), ("traces", ctypes.c_void_p),
+        ("trace_rows", ctypes.c_int32), ("it0", ctypes.c_int32), ("n_steps", ctypes.c_int32),
+    ]
+
+
 class _TTIPlan:
-    def __init__(self, cfg: TTIConfig, device, pitch: int):
+    """Device copies of a config's inputs; precision 8: everything in double
+    (parameters unrounded, exact float64 weights, float64 sponge and series)."""
+
+    def __init__(self, cfg: TTIConfig, device, pitch: int, precision: int = 4):
         torch = _torch()
         self.key = _tti_key(cfg, device, pitch)
         self.guard = InputGuard(config_inputs(cfg, _TTI_FIELDS))  # frozen while cached
         nx, ny, nz = cfg.dims
-        self.w2, self.w1 = tti_weights_f32(cfg.order)
+        f64 = precision == 8
+        tdt, ndt = (torch.float64, np.float64) if f64 else (torch.float32, np.float32)
+        self.w2, self.w1 = tti_weights_f64(cfg.order) if f64 else tti_weights_f32(cfg.order)
         self.params = []
-        for name, host in cfg.params().items():
-            t = torch.zeros((nx, ny, pitch), dtype=torch.float32, device=device)
+        for name, host in cfg.params(precision).items():
+            t = torch.zeros((nx, ny, pitch), dtype=tdt, device=device)
             t[:, :, :nz].copy_(host_tensor(host))
             self.params.append(t)
         self.sponge = None if cfg.sponge is None else tuple(
-            host_tensor(v).to(device) for v in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
+            host_tensor(np.asarray(v, dtype=ndt)).to(device)
+            for v in (cfg.sponge.x, cfg.sponge.y, cfg.sponge.z))
         self.series, self.src, self.n_series = None, (-1, 0, 0), 0
         if cfg.source is not None:
-            s = np.ascontiguousarray(np.asarray(cfg.source.series).astype(np.float32).reshape(-1))
+            # float32 samples (what the float32 path injects), converted exactly
+            # to double on the float64 path, as the acoustic float64 path does
+            s = np.ascontiguousarray(np.asarray(cfg.source.series).astype(np.float32)
+                                     .astype(ndt).reshape(-1))
             self.series = host_tensor(s).to(device)
             self.src = tuple(int(c) for c in cfg.source.location)
             self.n_series = int(s.size)
@@ -284,9 +330,13 @@ def tti_run(fld: TTIWavefield, cfg: TTIConfig, n_steps: Optional[int] = None,
     lib = _lib.load()
     dev = fld.device
     pitch_y = int(fld.p[0].shape[2])
-    plan = cached_plan(cfg, "_device_plan", _tti_key(cfg, dev, pitch_y),
-                       lambda: _TTIPlan(cfg, dev, pitch_y))
-    a = _TTIArgs()
+    f64 = fld.p[0].dtype == torch.float64
+    if f64 and variant not in ("auto", "direct"):
+        raise ValidationError("the float64 TTI path is the direct kernel (variant auto or direct)")
+    prec = 8 if f64 else 4
+    plan = cached_plan(cfg, "_device_plan64" if f64 else "_device_plan", _tti_key(cfg, dev, pitch_y),
+                       lambda: _TTIPlan(cfg, dev, pitch_y, prec))
+    a = _TTIArgs64() if f64 else _TTIArgs()
     a.abi_version = _lib.ABI_VERSION
     a.order = cfg.order
     a.nx, a.ny, a.nz = fld.dims
@@ -309,19 +359,24 @@ def tti_run(fld: TTIWavefield, cfg: TTIConfig, n_steps: Optional[int] = None,
     if plan.rec is not None:
         rows = max(cfg.n_t, fld.it + n)
         n_rec = cfg.receivers.count
-        if fld.traces is None or fld.traces.shape[0] < rows or fld.traces.shape[1] != n_rec:
-            fld.traces = grow_traces(fld, rows, n_rec, torch.float32, dev)
+        tdt = torch.float64 if f64 else torch.float32
+        if (fld.traces is None or fld.traces.shape[0] < rows or fld.traces.shape[1] != n_rec
+                or fld.traces.dtype != tdt):
+            fld.traces = grow_traces(fld, rows, n_rec, tdt, dev)
         a.n_rec = n_rec
         a.rec_xyz = plan.rec.data_ptr()
         a.traces = fld.traces.data_ptr()
         a.trace_rows = int(fld.traces.shape[0])
     a.it0 = fld.it
     a.n_steps = n
-    a.variant = _VARIANTS[variant]
-    a.interleaved = 1 if fld.interleaved else 0
     stream = torch.cuda.current_stream(dev).cuda_stream
     with torch.cuda.device(dev):
-        _lib.check(lib.fdr_tti_run(ctypes.byref(a), ctypes.c_void_p(stream)))
+        if f64:
+            _lib.check(lib.fdr_tti64_run(ctypes.byref(a), ctypes.c_void_p(stream)))
+        else:
+            a.variant = _VARIANTS[variant]
+            a.interleaved = 1 if fld.interleaved else 0
+            _lib.check(lib.fdr_tti_run(ctypes.byref(a), ctypes.c_void_p(stream)))
     for lv in (fld.p, fld.r):
         g = list(lv)
         lv[:] = [g[n % 3], g[(1 + n) % 3], g[(2 + n) % 3]]

@@ -137,3 +137,24 @@ def test_gpu_elastic_config5_grid_vs_c_oracle(el_mod):
     for k in FIELDS:
         assert sha(fld.numpy(k)) == sha(st.interior(k)), k
     assert (fld.traces.cpu().numpy() == st.traces).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [4, 8])
+def test_gpu_elastic_float64_path_vs_f64_oracle(order, cuda_device):
+    """fdr_elastic64_run (the direct kernels in double) against the independent
+    numpy float64 oracle."""
+    import torch
+
+    from paper_1608_03984_b200 import elastic
+    from paper_1608_03984_b200.errors import ValidationError
+
+    cfg = small_cfg(order=order, n_t=40)
+    fld = elastic.ElasticWavefield.allocate(cfg.dims, cfg.halo, dtype=torch.float64)
+    elastic.elastic_run(fld, cfg)
+    f64, tr64 = E.simulate_f64(cfg)
+    for k in FIELDS:
+        assert rel_l2(fld.numpy(k), f64[k]) < 1e-10, k
+    assert rel_l2(fld.traces.cpu().numpy()[: cfg.n_t], tr64) < 1e-10
+    with pytest.raises(ValidationError):
+        elastic.elastic_run(fld, cfg, 1, variant="queue")

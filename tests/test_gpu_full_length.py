@@ -175,7 +175,22 @@ def test_tti_config4_full_length(B, golden):
     if sha(traces) != g["traces"]["sha256"]:
         err = rel_l2(traces[:, ::g["trace_stride"]], samples["config4/traces"])
         pytest.fail(f"config4: traces differ (rel L2 on the sample {err:.3e})")
-    _record("config4", bitexact_vs_oracle=True, n_t=cfg.n_t)
+    # the float64 path (fdr_tti64_run) on the same model: the float32 error
+    p32, r32 = f.numpy("p"), f.numpy("r")
+    del f
+    torch.cuda.empty_cache()
+    f64 = tti.TTIWavefield.allocate(cfg.dims, cfg.halo, dtype=torch.float64)
+    tti.tti_run(f64, cfg)
+    e_p, e_r = rel_l2(p32, f64.numpy("p")), rel_l2(r32, f64.numpy("r"))
+    tr64 = f64.traces.cpu().numpy()[: cfg.n_t]
+    t_scale = float(np.abs(tr64).max())
+    e_tr = rel_l2(traces, tr64) if t_scale > 1e-30 else None
+    _record("config4", bitexact_vs_oracle=True, n_t=cfg.n_t, f32_rel_l2_vs_f64_p=e_p,
+            f32_rel_l2_vs_f64_r=e_r, f32_rel_l2_vs_f64_traces=e_tr, f64_traces_maxabs=t_scale)
+    del f64
+    torch.cuda.empty_cache()
+    assert e_p < 1e-3 and e_r < 1e-3
+    assert e_tr is None or e_tr < 1e-3
 
 
 def test_elastic_config5_full_length(B, golden):
@@ -205,4 +220,19 @@ def test_elastic_config5_full_length(B, golden):
     if sha(traces) != g["traces"]["sha256"]:
         err = rel_l2(traces[:, ::g["trace_stride"]], samples["config5/traces"])
         pytest.fail(f"config5: traces differ (rel L2 on the sample {err:.3e})")
-    _record("config5", bitexact_vs_oracle=True, n_t=cfg.n_t)
+    # the float64 path (fdr_elastic64_run) on the same model: the float32 error
+    f32 = {k: f.numpy(k) for k in elastic.FIELDS}
+    del f
+    torch.cuda.empty_cache()
+    f64 = elastic.ElasticWavefield.allocate(cfg.dims, cfg.halo, dtype=torch.float64)
+    elastic.elastic_run(f64, cfg)
+    errs = {k: rel_l2(f32[k], f64.numpy(k)) for k in elastic.FIELDS}
+    tr64 = f64.traces.cpu().numpy()[: cfg.n_t]
+    t_scale = float(np.abs(tr64).max())
+    e_tr = rel_l2(traces, tr64) if t_scale > 1e-30 else None
+    _record("config5", bitexact_vs_oracle=True, n_t=cfg.n_t,
+            f32_rel_l2_vs_f64_fields=errs, f32_rel_l2_vs_f64_traces=e_tr, f64_traces_maxabs=t_scale)
+    del f64
+    torch.cuda.empty_cache()
+    assert max(errs.values()) < 1e-3
+    assert e_tr is None or e_tr < 1e-3

@@ -177,3 +177,24 @@ def test_gpu_tti_config4_grid_vs_c_oracle(tti_mod):
     assert sha(fld.numpy("p")) == sha(st.interior("p"))
     assert sha(fld.numpy("r")) == sha(st.interior("r"))
     assert (fld.traces.cpu().numpy() == st.traces).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [4, 8])
+def test_gpu_tti_float64_path_vs_f64_oracle(tti_mod, order):
+    """fdr_tti64_run (the direct kernel in double) against the independent
+    numpy float64 paper-operator oracle: the same system to double precision."""
+    import torch
+
+    from paper_1608_03984_b200.errors import ValidationError
+
+    cfg = small_cfg(order=order, n_t=40)
+    fld = tti_mod.TTIWavefield.allocate(cfg.dims, cfg.halo, dtype=torch.float64)
+    tti_mod.tti_run(fld, cfg)
+    p64, r64, tr64 = T.simulate_f64(cfg)
+    assert fld.p[0].dtype == torch.float64 and fld.traces.dtype == torch.float64
+    assert rel_l2(fld.numpy("p"), p64) < 1e-10
+    assert rel_l2(fld.numpy("r"), r64) < 1e-10
+    assert rel_l2(fld.traces.cpu().numpy()[: cfg.n_t], tr64) < 1e-10
+    with pytest.raises(ValidationError):
+        tti_mod.tti_run(fld, cfg, 1, variant="queue")
