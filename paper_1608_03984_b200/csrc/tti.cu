@@ -937,9 +937,11 @@ void fill(TTIStep& s, const fdr_tti_args* a, int k) {
 
 static int run(const fdr_tti_args* a, cudaStream_t st) {
   int variant = a->variant;
+  // the streaming kernels index levels with 32-bit element offsets (twice
+  // the points for interleaved (p, r) levels)
+  const uint64_t elems = (uint64_t)a->nx * (uint64_t)a->pitch_x * (a->interleaved ? 2u : 1u);
   if (variant == FDR_VARIANT_AUTO)
-    variant = (a->order <= 8 && (uint64_t)a->nx * (uint64_t)a->pitch_x < (1ull << 32))
-                  ? FDR_VARIANT_QUEUE : FDR_VARIANT_DIRECT;
+    variant = (a->order <= 8 && elems < (1ull << 32)) ? FDR_VARIANT_QUEUE : FDR_VARIANT_DIRECT;
   if ((variant == FDR_VARIANT_QUEUE || variant == FDR_VARIANT_TMA) && a->n_steps > 0) {
     int rc = tti_stream_prepare(a);
     if (rc != FDR_OK) return rc;
