@@ -179,7 +179,10 @@ __global__ void tti_gather_kernel(const float* p, const int* rec, int n_rec, flo
 #ifndef FDR_TTI_TY
 #define FDR_TTI_TY 16
 #endif
-constexpr int TTZ = 32, TTY = FDR_TTI_TY, TNT = TTZ * TTY;
+#ifndef FDR_TTI_TZ
+#define FDR_TTI_TZ 32
+#endif
+constexpr int TTZ = FDR_TTI_TZ, TTY = FDR_TTI_TY, TNT = TTZ * TTY;
 constexpr int TMINB = TTY <= 8 ? 2 : 1;  // CTAs per SM the tile is sized for
 
 template <int R>
