@@ -747,7 +747,9 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
     src_l = a.sz - zb;
     qsrc = a.series[a.it];
   }
-  const size_t obase = (size_t)xb * a.pitch_x + (size_t)y * a.pitch_y + zb;
+  // 32-bit element offsets (the queue kernels take grids of < 2^32 elements)
+  const uint32_t px32 = (uint32_t)a.pitch_x;
+  const uint32_t obase = (uint32_t)xb * px32 + (uint32_t)y * (uint32_t)a.pitch_y + (uint32_t)zb;
 
   int slot = 0;
   uint32_t phase = 0;
@@ -872,7 +874,7 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
             else out[i].y = __fadd_rn(out[i].y, qsrc);
           }
         }
-        const size_t o = obase + (size_t)k * a.pitch_x;
+        const uint32_t o = obase + (uint32_t)k * px32;
 #pragma unroll
         for (int i = 0; i < NO; ++i) {
           float* dst = a.f[(PASS == 0 ? VX : SXX) + i] + o;
