@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(QNT, 2)
     __syncwarp();
     if (fdr::elect_one() && arrive_is_last_a(af + 8u * G::NS)) {
       fdr::mbar_wait_a(af + 8u * G::NS, phase);
+      fence_proxy_async();  // generic-proxy reads of the stage before the TMA refill (cross-proxy WAR)
       if (p + G::NS < nplanes) issue(p + G::NS, slot);
     }
     ac += SB;

@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(TB_NT + 32, 2)
     for (int t = 0; t < nst; ++t) {
       // stage t read by every compute warp: refill it with stream plane t + NA
       mbar_wait(&emptyA[slot], ph);
+      fence_proxy_async();  // the warps' generic reads of the stage before the TMA refill
       if (t + G::NA < nst) issueA(t + G::NA, slot);
       // A of plane t - 2R stored by every compute warp: publish the progress
       mbar_wait(&doneA[slot], ph);
@@ -344,7 +345,10 @@ __global__ void __launch_bounds__(TB_NT + 32, 2)
       // halo owner's A has passed it (the first NB planes: no earlier use)
       const int pb = t - 3 * R - G::D, q = pb + G::NB;
       if (q >= 0 && q < nx) {
-        if (pb >= 0) mbar_wait(&emptyB[pb % G::NB], (uint32_t)(pb / G::NB) & 1u);
+        if (pb >= 0) {
+          mbar_wait(&emptyB[pb % G::NB], (uint32_t)(pb / G::NB) & 1u);
+          fence_proxy_async();  // as above, for ring B
+        }
 #if FDR_TB2_WAIT
         if (!tb2_wait(run, nb, nnb, run.base + (unsigned)q + 1u)) atomicAdd_system(run.err, 1u);
 #endif

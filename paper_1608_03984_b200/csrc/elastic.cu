@@ -455,6 +455,7 @@ __global__ void __launch_bounds__(ENT, EMINB) el_stream(const __grid_constant__ 
       __syncwarp();
       if (leader && el_arrive_last(&empty[slot])) {
         mbar_wait(&empty[slot], phase);
+        fence_proxy_async();  // generic-proxy reads of the stage before the TMA refill (cross-proxy WAR)
         if (pl + G::NS < nplanes) issue(pl + G::NS, slot);
       }
       if (++slot == G::NS) {
@@ -844,6 +845,7 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
       __syncwarp();
       if (elect_one() && el_arrive_last_a(af + 8u * G::NS)) {
         mbar_wait_a(af + 8u * G::NS, phase);
+        fence_proxy_async();  // generic-proxy reads of the stage before the TMA refill (cross-proxy WAR)
         if (pl + G::NS < nplanes) issue(pl + G::NS, slot);
       }
       if (CA) {

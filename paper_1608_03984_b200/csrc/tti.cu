@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_stream(const __grid_constant__
       __syncwarp();
       if (leader && mbar_arrive_last(&empty[slot])) {
         mbar_wait(&empty[slot], phase);
+        fence_proxy_async();  // generic-proxy reads of the stage before the TMA refill (cross-proxy WAR)
         if (p + G::NS < nplanes) issue(p + G::NS, slot);
       }
       if (++slot == G::NS) {
@@ -745,6 +746,7 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
       if (CA ? (elect_one() && mbar_arrive_last_a(af + 8u * G::NS))
              : (leader && mbar_arrive_last(&empty[slot]))) {
         if (CA) mbar_wait_a(af + 8u * G::NS, phase); else mbar_wait(&empty[slot], phase);
+        fence_proxy_async();  // generic-proxy reads of the stage before the TMA refill (cross-proxy WAR)
         if (p + G::NS < nplanes) issue(p + G::NS, slot);
       }
       if (CA) {
