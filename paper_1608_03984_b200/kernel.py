@@ -37,7 +37,8 @@ from .stencils import abs_sum, acoustic_weights_f32, second_derivative_weights
 
 _VARIANTS = {"auto": _lib.VARIANT_AUTO, "direct": _lib.VARIANT_DIRECT, "tma": _lib.VARIANT_TMA,
              "queue": _lib.VARIANT_QUEUE, "persistent": _lib.VARIANT_PERSISTENT,
-             "cluster": _lib.VARIANT_CLUSTER, "tb2": _lib.VARIANT_TB2}
+             "cluster": _lib.VARIANT_CLUSTER, "tb2": _lib.VARIANT_TB2,
+             "fma": _lib.VARIANT_FMA}  # fma: contracted taps, opt-in, NOT bit-exact
 
 
 def _torch():
@@ -541,7 +542,7 @@ def _run_f64(fld: Wavefield, cfg: KernelConfig, n: int, variant: str) -> Wavefie
     torch = _torch()
     lib = _lib.load()
     dev = fld.device
-    if variant in ("persistent", "cluster", "tb2"):
+    if variant in ("persistent", "cluster", "tb2", "fma"):
         raise ValidationError("the float64 path has variants auto, queue, tma and direct")
     if isinstance(cfg.source, OffGridSource) or isinstance(cfg.receivers, OffGridReceivers):
         raise ValidationError("the float64 path takes on-grid sources and receivers")
