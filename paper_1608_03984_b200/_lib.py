@@ -108,6 +108,9 @@ EXPORTS = (
     ("fdr_last_error", ctypes.c_char_p, ()),
     ("fdr_device_count", ctypes.c_int, ()),
     ("fdr_acoustic_run", ctypes.c_int, (ctypes.POINTER(AcousticArgs), _vp)),
+    ("fdr_acoustic_slabs_run", ctypes.c_int,
+     (ctypes.POINTER(AcousticArgs), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+      ctypes.POINTER(ctypes.c_void_p))),
     ("fdr_acoustic_oracle_step", ctypes.c_int,
      (ctypes.POINTER(AcousticArgs), ctypes.POINTER(ctypes.c_double), ctypes.c_double,
       ctypes.c_double, _vp, _vp)),

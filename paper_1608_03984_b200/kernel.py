@@ -440,6 +440,36 @@ def _fill_args(args: _lib.AcousticArgs, cfg: KernelConfig, plan: _DevicePlan, di
     args.variant = variant
 
 
+def device_args(fld: Wavefield, cfg: KernelConfig, n: int, variant: str = "auto") -> "_lib.AcousticArgs":
+    """The fdr_acoustic_args of n float32 steps of `fld` under `cfg` (device
+    plan built or reused, trace buffer grown); the caller launches them."""
+    torch = _torch()
+    dev = fld.device
+    pitch_y = int(fld.grids[0].shape[2])
+    pitch_x = int(fld.grids[0].shape[1]) * pitch_y
+    plan = _plan(cfg, dev, pitch_y)
+    args = _lib.AcousticArgs()
+    _fill_args(args, cfg, plan, fld.dims, pitch_y, pitch_x, fld.it, n, _VARIANTS[variant])
+    args.m = _ptr(plan.m_grid)
+    args.rec_w = _ptr(plan.rec_w)
+    args.src_w = _ptr(plan.src_w)
+    for i in range(3):
+        args.levels[i] = fld.grids[i].data_ptr()
+    if plan.sponge is not None:
+        args.sponge_x, args.sponge_y, args.sponge_z = (p.data_ptr() for p in plan.sponge)
+    args.series = _ptr(plan.series)
+    if plan.rec is not None:
+        rows = max(cfg.n_t, fld.it + n)
+        n_rec = cfg.receivers.count
+        if fld.traces is None or fld.traces.shape[1] != n_rec or fld.traces.shape[0] < rows:
+            fld.traces = grow_traces(fld, rows, n_rec, torch.float32, dev)
+        args.rec_xyz = plan.rec.data_ptr()
+        args.traces = fld.traces.data_ptr()
+        args.trace_rows = int(fld.traces.shape[0])
+    args._keep = plan  # the plan's device buffers outlive the call
+    return args
+
+
 def run(fld: Wavefield, cfg: KernelConfig, n_steps: Optional[int] = None,
         variant: str = "auto") -> Wavefield:
     """Advance `n_steps` (default cfg.n_t) steps in one library call.
@@ -467,27 +497,7 @@ def run(fld: Wavefield, cfg: KernelConfig, n_steps: Optional[int] = None,
                                   "tensors of one shape and dtype")
     if dt0 == torch.float64:
         return _run_f64(fld, cfg, n, variant)
-    pitch_y = int(fld.grids[0].shape[2])
-    pitch_x = int(fld.grids[0].shape[1]) * pitch_y
-    plan = _plan(cfg, dev, pitch_y)
-    args = _lib.AcousticArgs()
-    _fill_args(args, cfg, plan, fld.dims, pitch_y, pitch_x, fld.it, n, _VARIANTS[variant])
-    args.m = _ptr(plan.m_grid)
-    args.rec_w = _ptr(plan.rec_w)
-    args.src_w = _ptr(plan.src_w)
-    for i in range(3):
-        args.levels[i] = fld.grids[i].data_ptr()
-    if plan.sponge is not None:
-        args.sponge_x, args.sponge_y, args.sponge_z = (p.data_ptr() for p in plan.sponge)
-    args.series = _ptr(plan.series)
-    if plan.rec is not None:
-        rows = max(cfg.n_t, fld.it + n)
-        n_rec = cfg.receivers.count
-        if fld.traces is None or fld.traces.shape[1] != n_rec or fld.traces.shape[0] < rows:
-            fld.traces = grow_traces(fld, rows, n_rec, torch.float32, dev)
-        args.rec_xyz = plan.rec.data_ptr()
-        args.traces = fld.traces.data_ptr()
-        args.trace_rows = int(fld.traces.shape[0])
+    args = device_args(fld, cfg, n, variant)
     stream = torch.cuda.current_stream(dev).cuda_stream
     with torch.cuda.device(dev):
         _lib.check(lib.fdr_acoustic_run(ctypes.byref(args), ctypes.c_void_p(stream)))

@@ -29,7 +29,10 @@ weights are unchanged.
 The result is bit-identical to the single-grid run: the same arithmetic on the
 same values at every owned point.  `SlabPlan` and the exchange are plain host
 logic (tests/test_slab.py runs them with the numpy oracle on gloo ranks);
-`run_slab` is the GPU path (NCCL point-to-point of plane blocks over NVLink).
+`run_slab` is the multi-process GPU path (NCCL point-to-point of plane blocks
+over NVLink); `run_slabs` drives every slab of one process through the
+library's own exchange (fdr_acoustic_slabs_run: boundary planes first, peer
+copies into the neighbours' ghost planes overlapped with the interior planes).
 """
 
 from dataclasses import dataclass
@@ -231,3 +234,46 @@ def gather_slabs(fld, plan: SlabPlan, rank: int, dims, group=None):
     if tuple(full.shape) != tuple(dims):
         raise ValidationError("gathered slabs do not tile the grid")
     return full
+
+
+def run_slabs(cfg: KernelConfig, plan: SlabPlan, devices=None, n_steps: Optional[int] = None):
+    """All slabs of `plan` in one process through the library's exchange
+    (fdr_acoustic_slabs_run): slab i on devices[i] (default: every slab on
+    the current device), each step's boundary planes computed first and
+    copied into the neighbours' ghost planes (cudaMemcpyPeerAsync; NVLink
+    between devices) while the interior planes are computed.  On-grid source
+    and receivers (ghost width r).  Returns (global final level as numpy,
+    global traces or None), like run_slabs_local."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from . import kernel as K
+
+    if isinstance(cfg.source, OffGridSource) or isinstance(cfg.receivers, OffGridReceivers):
+        raise ValidationError("run_slabs takes on-grid sources and receivers (run_slab / "
+                              "run_slabs_local take off-grid ones)")
+    if plan.halo != cfg.halo:
+        raise ValidationError(f"run_slabs needs ghost width r = {cfg.halo}, plan has {plan.halo}")
+    n = cfg.n_t if n_steps is None else int(n_steps)
+    ns = plan.n_slabs
+    if devices is None:
+        devices = [torch.cuda.current_device()] * ns
+    if len(devices) != ns:
+        raise ValidationError("one device per slab")
+    parts = [slab_config(cfg, plan, i) for i in range(ns)]
+    flds = [K.Wavefield.allocate(c.dims, c.halo, torch.device("cuda", d))
+            for (c, _), d in zip(parts, devices)]
+    if n == 0:
+        return gather_local(cfg, plan, parts, flds)
+    keep = [K.device_args(f, c, n) for (c, _), f in zip(parts, flds)]
+    arr = (_lib.AcousticArgs * ns)(*keep)
+    devs = (ctypes.c_int * ns)(*[int(d) for d in devices])
+    streams = (ctypes.c_void_p * ns)(*[torch.cuda.current_stream(d).cuda_stream for d in devices])
+    _lib.check(_lib.load().fdr_acoustic_slabs_run(arr, ns, devs, streams))
+    for f in flds:
+        g = f.grids
+        f.grids = [g[n % 3], g[(1 + n) % 3], g[(2 + n) % 3]]
+        f.it += n
+    return gather_local(cfg, plan, parts, flds)

@@ -147,3 +147,39 @@ def test_gpu_slabs_local_bitexact(cuda_device, n_slabs):
         B.run(fld, cfg, n)
         assert np.array_equal(got, fld.numpy())
         assert np.array_equal(traces[:n], fld.traces.cpu().numpy()[:n])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_slabs", [1, 2, 3, 5])
+def test_gpu_library_slabs_bitexact(cuda_device, n_slabs):
+    """fdr_acoustic_slabs_run (the library's exchange: boundary planes first,
+    peer copies into the neighbours' ghost planes overlapped with the interior)
+    on one device == the single-grid run, field and traces."""
+    import paper_1608_03984_b200 as B
+    from paper_1608_03984_b200.slab import run_slabs
+
+    for name, (cfg, n) in slab_case().items():
+        if name.startswith("off"):
+            continue
+        plan = SlabPlan(cfg.dims[0], n_slabs, cfg.halo)
+        got, traces = run_slabs(cfg, plan, n_steps=n)
+        fld = B.Wavefield.allocate(cfg.dims, cfg.halo)
+        B.run(fld, cfg, n)
+        assert np.array_equal(got, fld.numpy()), name
+        assert np.array_equal(traces[:n], fld.traces.cpu().numpy()[:n]), name
+
+
+@pytest.mark.gpu
+def test_gpu_library_slabs_full_size(cuda_device):
+    """Config-2 grid (512^3, order 8) split in 4 x-slabs on one device for 20
+    steps from zero with the Ricker source: identical to the single-grid run."""
+    import paper_1608_03984_b200 as B
+    from paper_1608_03984_b200.slab import run_slabs
+    from paper_1608_03984_b200.synthetic import config2
+
+    cfg = config2(order=8, n_t=20)
+    got, traces = run_slabs(cfg, SlabPlan(cfg.dims[0], 4, cfg.halo))
+    fld = B.Wavefield.allocate(cfg.dims, cfg.halo)
+    B.run(fld, cfg)
+    assert np.array_equal(got, fld.numpy())
+    assert np.array_equal(traces[:20], fld.traces.cpu().numpy()[:20])
