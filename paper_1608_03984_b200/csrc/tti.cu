@@ -488,6 +488,27 @@ constexpr bool TTI_CARRY = FDR_TTI_CARRY != 0;
 #else
 constexpr bool TTI_CARRY = true;
 #endif
+// Deferred dyz: plane p's D1z rows are consumed at iteration p + 1, so the
+// wait for every warp's rows has a whole plane of slack (ncu: the per-plane
+// wait on the D1z-ready barrier was the top stall; the 8 warps with halo rows
+// arrive late every plane).  The rows live in the stage's D1z area, which TMA
+// never writes, so releasing the stage at the end of iteration p stays safe;
+// the area is rewritten at iteration p + NS, after every warp has arrived on
+// the barrier of plane p + 2 (waited at p + 3), i.e. after its reads at p + 1.
+#ifdef FDR_TTI_DEFER
+constexpr bool TTI_DEFER = FDR_TTI_DEFER != 0;
+#else
+constexpr bool TTI_DEFER = true;
+#endif
+// With DEFER: the halo D1z rows (2R of them per plane) rotate over groups of
+// 2R warps plane by plane instead of always falling to warps 0 .. 2R-1, so
+// every warp does the same work over NG planes and the one-plane slack of the
+// deferred wait absorbs the per-plane difference.
+#ifdef FDR_TTI_HALT
+constexpr bool TTI_HALT = FDR_TTI_HALT != 0;
+#else
+constexpr bool TTI_HALT = true;
+#endif
 
 // D1z of an interleaved (p, r) row from the 32-bit shared address of the
 // own pair: one 8-byte load per tap
@@ -573,7 +594,13 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
   const bool ok = y < a.ny && z < a.nz;
   const int bown = (ty + R) * G::BZ + G::LZ + tz;
   const int town = ty * TTZ + tz;
-  const int hrow = ty < R ? ty : (ty < 2 * R ? TTY + ty : -1);
+  constexpr bool DEFER = TTI_DEFER && TTI_CARRY && G::NS >= 4;
+  constexpr int HG = 2 * R, NG = TTY / HG;  // halo-row warp groups (ALT)
+  constexpr bool ALT = DEFER && TTI_HALT && NG >= 2;
+  const int hgrp = ty / HG, hh = ty % HG;
+  const int hrow = ALT ? (hgrp < NG ? (hh < R ? hh : TTY + hh) : -1)
+                       : (ty < R ? ty : (ty < 2 * R ? TTY + ty : -1));
+  int hturn = 0;  // ALT: the group computing the halo rows of this plane
   float gy = 1.0f, gz = 1.0f;
   if (SPONGE && ok) {
     gy = a.gy[y];
@@ -618,6 +645,16 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
   uint32_t ah = smem_u32(smem + G::O_BP + (IL ? 2 : 1) * (hr0 * G::BZ + G::LZ + tz));
   uint32_t ahdz = smem_u32(smem + G::O_DZP + 2 * (hr0 * TTZ + tz));
   uint32_t af = smem_u32(full);  // full[slot]; empty[] and dzrdy[] follow
+  // DEFER: the previous plane's D1z rows (own address), barrier, parity and cyz
+  uint32_t adzp = 0, afp = 0, phasep = 0;
+  float cyzp = 0.0f;
+  auto dyz_at = [&](uint32_t adr) {
+    auto ldz = [&](int rows) { return lds64a(adr + 8 * rows * TTZ); };
+    f2 d = mul2(bcast(a.w1[1]), sub2(ldz(1), ldz(-1)));
+#pragma unroll
+    for (int j = 2; j <= R; ++j) d = fma2(bcast(a.w1[j]), sub2(ldz(j), ldz(-j)), d);
+    return d;
+  };
 #pragma unroll 1
   for (int p0 = 0; p0 < nplanes; p0 += G::U) {
 #pragma unroll
@@ -652,7 +689,7 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
       float* dzb = st + G::O_DZP;  // interleaved (p, r) D1z rows, 2 * BY * TTZ floats
       if (CA) {
         sts64a(adz, dz1);
-        if (hrow >= 0) sts64a(ahdz, IL ? d1_row2i<R>(ah, a.w1) : d1_row2a<R>(ah, DR, a.w1));
+        if (ALT ? hgrp == hturn : hrow >= 0) sts64a(ahdz, IL ? d1_row2i<R>(ah, a.w1) : d1_row2a<R>(ah, DR, a.w1));
       } else {
         *reinterpret_cast<f2*>(dzb + 2 * ((ty + R) * TTZ + tz)) = dz1;
         if (hrow >= 0)
@@ -675,6 +712,15 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
       if (CA ? elect_one() : leader) {
         if (CA) mbar_arrive_ta(af + 16u * G::NS); else mbar_arrive_t(&dzrdy[slot]);
       }
+      // DEFER: dyz of the previous plane completes its G partial sum
+      // (gin = fma(cyz, dyz, ...)); at R = 1 the update below needs it
+      auto deferred = [&]() {
+        if (p > 0) {
+          mbar_wait_a(afp + 16u * G::NS, phasep);
+          gq[QI(R + u - 1 + (ROT ? PER : 0))] = fma2(bcast(cyzp), dyz_at(adzp), gq[QI(R + u - 1 + (ROT ? PER : 0))]);
+        }
+      };
+      if constexpr (DEFER && R == 1) deferred();
       // ---- the plane R behind: x derivatives and the update
       const int k = p - 2 * R;
       if (k >= 0) {
@@ -729,9 +775,12 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
           }
         }
       }
+      if constexpr (DEFER) {
+        if constexpr (R > 1) deferred();
+        cyzp = lt(G::O_IN + 2 * G::TILE);  // this plane's cyz, read before the stage is released
+      } else {
       // the D1z rows are complete
       if (CA) mbar_wait_a(af + 16u * G::NS, phase); else mbar_wait(&dzrdy[slot], phase);
-      {
         const float* db = dzb + 2 * ((ty + R) * TTZ + tz);
         auto ldz = [&](int rows) {
           return CA ? lds64a(adz + 8 * rows * TTZ) : *reinterpret_cast<const f2*>(db + 2 * rows * TTZ);
@@ -748,6 +797,14 @@ __global__ void __launch_bounds__(TNT, TMINB) tti_pack(const __grid_constant__ T
         if (CA) mbar_wait_a(af + 8u * G::NS, phase); else mbar_wait(&empty[slot], phase);
         fence_proxy_async();  // generic-proxy reads of the stage before the TMA refill (cross-proxy WAR)
         if (p + G::NS < nplanes) issue(p + G::NS, slot);
+      }
+      if constexpr (DEFER) {
+        adzp = adz;
+        afp = af;
+        phasep = phase;
+      }
+      if constexpr (ALT) {
+        if (++hturn == NG) hturn = 0;
       }
       if (CA) {
         ab += SB; at += SB; adz += SB; ah += SB; ahdz += SB; af += 8u;
