@@ -21,7 +21,7 @@ MAX_RADIUS = 16
 FDR_OK, FDR_EINVAL, FDR_ECUDA = 0, -1, -2
 M_NONE, M_SCALAR, M_GRID = 0, 1, 2
 (VARIANT_AUTO, VARIANT_DIRECT, VARIANT_TMA, VARIANT_QUEUE, VARIANT_PERSISTENT, VARIANT_CLUSTER,
- VARIANT_TB2, VARIANT_FMA) = (0, 1, 2, 3, 4, 5, 6, 7)
+ VARIANT_TB2, VARIANT_FMA, VARIANT_QUEUE2) = (0, 1, 2, 3, 4, 5, 6, 7, 8)
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32

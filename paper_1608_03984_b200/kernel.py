@@ -38,7 +38,8 @@ from .stencils import abs_sum, acoustic_weights_f32, second_derivative_weights
 _VARIANTS = {"auto": _lib.VARIANT_AUTO, "direct": _lib.VARIANT_DIRECT, "tma": _lib.VARIANT_TMA,
              "queue": _lib.VARIANT_QUEUE, "persistent": _lib.VARIANT_PERSISTENT,
              "cluster": _lib.VARIANT_CLUSTER, "tb2": _lib.VARIANT_TB2,
-             "fma": _lib.VARIANT_FMA}  # fma: contracted taps, opt-in, NOT bit-exact
+             "fma": _lib.VARIANT_FMA,  # fma: contracted taps, opt-in, NOT bit-exact
+             "queue2": _lib.VARIANT_QUEUE2}  # queue kernel, two y rows per thread
 
 
 def _torch():

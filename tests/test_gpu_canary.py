@@ -73,6 +73,7 @@ def _acoustic_cfg(B, order, dims, steps=4):
 
 @pytest.mark.parametrize("variant,order,dims", [
     ("queue", 8, (40, 37, 45)), ("queue", 16, (36, 35, 41)), ("queue", 2, (20, 19, 23)),
+    ("queue2", 8, (40, 37, 45)), ("queue2", 16, (36, 35, 41)), ("queue2", 2, (20, 19, 23)),
     ("tma", 8, (40, 37, 45)), ("direct", 6, (20, 19, 23)), ("persistent", 4, (24, 21, 27)),
     ("cluster", 4, (32, 30, 34)), ("tb2", 4, (40, 37, 45)), ("tb2", 8, (36, 35, 41))])
 def test_acoustic_canaries_and_determinism(B, variant, order, dims):

@@ -14,7 +14,7 @@ from cases import random_levels, sha
 
 pytestmark = pytest.mark.gpu
 
-ACOUSTIC_VARIANTS = ["queue", "tma", "direct", "persistent", "cluster"]
+ACOUSTIC_VARIANTS = ["queue", "queue2", "tma", "direct", "persistent", "cluster"]
 
 
 @pytest.fixture(scope="module")

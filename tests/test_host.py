@@ -252,6 +252,6 @@ def test_tb2_variant_is_known_to_the_library():
         _lib.check(_lib.load().fdr_acoustic_run(ctypes.byref(args), None))
     args.nx = args.ny = args.nz = 16
     args.pitch_y, args.pitch_x = 16, 256
-    args.variant = _lib.VARIANT_FMA + 1
+    args.variant = _lib.VARIANT_QUEUE2 + 1
     with pytest.raises(B.ValidationError, match="unknown variant"):
         _lib.check(_lib.load().fdr_acoustic_run(ctypes.byref(args), None))

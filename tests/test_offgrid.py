@@ -61,7 +61,7 @@ def test_validation():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", ["auto", "queue", "tma", "direct"])
+@pytest.mark.parametrize("variant", ["auto", "queue", "queue2", "tma", "direct"])
 def test_gpu_offgrid_bitexact_vs_oracle(cuda_device, variant):
     cfg = offgrid_case()
     fld = B.Wavefield.allocate(cfg.dims, cfg.halo)
