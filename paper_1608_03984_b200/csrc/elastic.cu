@@ -14,7 +14,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "../../include/b200fd.h"
 #include "fdr_common.cuh"
@@ -45,6 +47,11 @@ struct ElStep {
   float* traces;
   int gather_row;
   int chunk;
+  // x range of this launch (the whole grid except in the windowed schedule,
+  // el_window_step) and whether the velocity stores stay in L2 (plain stores
+  // instead of streaming ones) for the stress launch that follows closely
+  int x0, x1;
+  int keep_v;
 };
 
 __device__ __forceinline__ float at(const float* u, const ElStep& a, int x, int y, int z) {
@@ -79,6 +86,7 @@ __device__ void gather_vz(const ElStep& a) {
   const int stride = nthr * (int)(gridDim.x * gridDim.y * gridDim.z);
   for (int i = b * nthr + t; i < a.n_rec; i += stride) {
     const int* q = a.rec + 3 * i;
+    if (q[0] < a.x0 || q[0] >= a.x1) continue;  // another window's launch samples it
     a.traces[(size_t)a.gather_row * a.n_rec + i] =
         a.f[VZ][(size_t)q[0] * a.pitch_x + (size_t)q[1] * a.pitch_y + q[2]];
   }
@@ -156,7 +164,15 @@ __global__ void __launch_bounds__(256) el_str_direct(const ElStep a) {
   } while (0)
 
 int el_stream_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, int* chunk_cache);
-int el_queue_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, int* chunk_cache);
+// Per-run state of the queue path: the x-chunk choice and, for the fused
+// schedule, the ticket/flag buffer (stream-ordered allocation) and step count.
+struct ElRunState {
+  int chunk = 0;
+  unsigned* fuse_buf = nullptr;
+  int fuse_step = 0;
+};
+int el_queue_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, ElRunState* rs);
+void el_queue_refresh_knobs();
 
 static int validate(const fdr_elastic_args* a) {
   if (!a) return fail(FDR_EINVAL, "args is NULL");
@@ -216,6 +232,8 @@ static void fill(ElStep& s, const fdr_elastic_args* a, int k) {
   // receivers sample vz at the start of the stress pass (vz is final for
   // step `it` there and the stress pass does not write it)
   s.gather_row = (a->n_rec > 0 && a->traces && s.it < a->trace_rows) ? s.it : -1;
+  s.x0 = 0;
+  s.x1 = a->nx;
 }
 
 static int run(const fdr_elastic_args* a, cudaStream_t st) {
@@ -225,12 +243,21 @@ static int run(const fdr_elastic_args* a, cudaStream_t st) {
     variant = (a->order <= 8 && small_index) ? FDR_VARIANT_QUEUE : FDR_VARIANT_DIRECT;
   if ((variant == FDR_VARIANT_QUEUE || variant == FDR_VARIANT_TMA) && (!small_index || a->order > 8))
     return fail(FDR_EINVAL, "the elastic streaming kernels need order <= 8 and < 2^32 elements");
-  int chunk = 0;
+  ElRunState rs;
+  int& chunk = rs.chunk;
+  if (variant == FDR_VARIANT_QUEUE) el_queue_refresh_knobs();
+  struct FreeFuse {  // the fused schedule's buffer goes back in stream order
+    ElRunState& r;
+    cudaStream_t st;
+    ~FreeFuse() {
+      if (r.fuse_buf) cudaFreeAsync(r.fuse_buf, st);
+    }
+  } free_fuse{rs, st};
   for (int k = 0; k < a->n_steps; ++k) {
     ElStep s;
     fill(s, a, k);
     if (variant == FDR_VARIANT_QUEUE) {  // el_queue (production)
-      int rc = el_queue_step(s, a, st, &chunk);
+      int rc = el_queue_step(s, a, st, &rs);
       if (rc != FDR_OK) return rc;
     } else if (variant == FDR_VARIANT_TMA) {  // el_stream (previous design)
       int rc = el_stream_step(s, a, st, &chunk);
@@ -671,23 +698,18 @@ FDR_DEV void stg2cs(float* p, float2 v) {
 #ifndef FDR_EL_CARRY_STRESS
 #define FDR_EL_CARRY_STRESS 0
 #endif
+// One (tile, x range) of a pass: the whole work of an el_queue CTA, also the
+// item of the fused persistent kernel (el_fused), which re-initialises the
+// ring's mbarriers for every item (`reinit`).
 template <int R, int PASS, bool SPONGE>
-#ifndef FDR_EL_MINB
-#define FDR_EL_MINB 2
-#endif
-__global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constant__ ElQMaps maps, const ElStep a) {
+FDR_DEV void el_queue_body(const ElQMaps& maps, const ElStep& a, const int zt, const int yt,
+                           const int xb, const int xe, float* smem, const bool reinit) {
   using G = QGeoE<R, PASS>;
   constexpr int LZ = G::LZ;
-  extern __shared__ __align__(128) float smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::NS * G::STAGE);
   uint64_t* empty = full + G::NS;
-  if (PASS == 1) gather_vz(a);
   const int tid = threadIdx.x;
   const int tz = tid % QNZ, ty = tid / QNZ;
-  const int zt = blockIdx.x * QZ, yt = blockIdx.y * QY;
-  const int xb = blockIdx.z * a.chunk;
-  const int xe = min(a.nx, xb + a.chunk);
-  if (xb >= xe) return;
   const int n = xe - xb;
   const int nplanes = n + 2 * R;
 
@@ -713,6 +735,10 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
   if (tid == 0) {
     for (int f = 0; f < 3; ++f) prefetch_tensormap(&maps.win[f]);
     for (int sl = 0; sl < G::NS; ++sl) {
+      if (reinit) {
+        mbar_inval(&full[sl]);
+        mbar_inval(&empty[sl]);
+      }
       mbar_init(&full[sl], 1);
       mbar_init(&empty[sl], G::NWARPS);
     }
@@ -880,7 +906,10 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
 #pragma unroll
         for (int i = 0; i < NO; ++i) {
           float* dst = a.f[(PASS == 0 ? VX : SXX) + i] + o;
-          if (vec_ok) stg2cs(dst, out[i]);
+          if (vec_ok) {
+            if (PASS == 0 && a.keep_v) *reinterpret_cast<float2*>(dst) = out[i];
+            else stg2cs(dst, out[i]);
+          }
           else if (row_ok && zb < a.nz) dst[0] = out[i].x;
         }
       }
@@ -894,6 +923,165 @@ __global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constan
       }
     }
   }
+}
+
+template <int R, int PASS, bool SPONGE>
+#ifndef FDR_EL_MINB
+#define FDR_EL_MINB 2
+#endif
+__global__ void __launch_bounds__(QN, FDR_EL_MINB) el_queue(const __grid_constant__ ElQMaps maps, const ElStep a) {
+  extern __shared__ __align__(128) float smem[];
+  if (PASS == 1) gather_vz(a);
+  const int xb = a.x0 + blockIdx.z * a.chunk;
+  const int xe = min(a.x1, xb + a.chunk);
+  if (xb >= xe) return;
+  el_queue_body<R, PASS, SPONGE>(maps, a, blockIdx.x * QZ, blockIdx.y * QY, xb, xe, smem, false);
+}
+
+// ============================================================ fused step
+// el_fused: one persistent launch per time step runs both passes as items
+// (pass, window k of C x-planes, tile t) handed out by a ticket counter, so the
+// stress item of a window finds the new velocities and the stresses of its
+// window still in L2 (windowed schedule above, without the launches).
+//   - Ticket order: the velocity items in (k, t) order; the stress items in
+//     the same order, each placed `lag` velocity items after V(k+1, t), i.e.
+//     after every velocity item it depends on was handed out.
+//   - S(k, t) reads the new velocities of windows k-1 .. k+1 on its tile's halo
+//     and overwrites the stresses those velocity items read: it waits until
+//     V(k-1 .. k+1) of the tile and its 8 neighbours have published (a stamp
+//     per velocity item, st.release.gpu after the CTA's stores; relaxed polls +
+//     fence.acq_rel.gpu + fence.proxy.async.global before the TMA reads).
+//   - Velocity items wait for nothing: their inputs are final since the previous
+//     launch.  Every dependency points to an earlier ticket and a CTA takes its
+//     tickets in order, so the schedule cannot deadlock; a wait that exceeds
+//     wait_cycles gives up and reports through the error word.
+struct ElFuse {
+  unsigned* ticket;   // monotonic across the run's launches
+  unsigned base;      // ticket value of this launch's item 0
+  unsigned* flags;    // [K][T] stamp of the last launch that finished V(k, t)
+  unsigned stamp;     // this launch's stamp
+  int C, K, T, tzn, tyn, lag;
+  long long wait_cycles;
+  unsigned* err;
+};
+
+FDR_DEV unsigned el_ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int R, bool SPONGE>
+__global__ void __launch_bounds__(QN, FDR_EL_MINB)
+    el_fused(const __grid_constant__ ElQMaps mv, const __grid_constant__ ElQMaps ms, const ElStep a,
+             const ElFuse f) {
+  extern __shared__ __align__(128) float smem[];
+  __shared__ int item[3];  // pass (-1: no more items), window, tile
+  const int NV = f.K * f.T, P = f.T + f.lag, total = 2 * NV;
+  for (bool first = true;; first = false) {
+    if (threadIdx.x == 0) {
+      const int tk = (int)(atomicAdd(f.ticket, 1u) - f.base);
+      int pass = -1, idx = 0;
+      if (tk < total) {
+        if (tk < P) {
+          pass = 0;
+          idx = tk;
+        } else {
+          const int j = tk - P, rem = NV - P;
+          if (j < 2 * rem) {
+            pass = (j & 1) ? 0 : 1;
+            idx = (j & 1) ? P + (j >> 1) : (j >> 1);
+          } else {
+            pass = 1;
+            idx = rem + (j - 2 * rem);
+          }
+        }
+      }
+      const int k = idx / f.T, t = idx - k * f.T;
+      if (pass == 1) {
+        const int tzi = t % f.tzn, tyi = t / f.tzn;
+        long long t0 = 0;
+        for (int spin = 0;; ++spin) {
+          bool all = true;
+          for (int dk = -1; dk <= 1; ++dk) {
+            const int kk = k + dk;
+            if (kk < 0 || kk >= f.K) continue;
+            for (int dy = -1; dy <= 1; ++dy) {
+              const int yy = tyi + dy;
+              if (yy < 0 || yy >= f.tyn) continue;
+#pragma unroll
+              for (int dz = -1; dz <= 1; ++dz) {
+                const int zz = tzi + dz;
+                if (zz < 0 || zz >= f.tzn) continue;
+                all &= el_ld_relaxed(f.flags + (size_t)kk * f.T + yy * f.tzn + zz) == f.stamp;
+              }
+            }
+          }
+          if (all) break;
+          if (spin == 0) t0 = clock64();
+          else if (clock64() - t0 > f.wait_cycles) {
+            atomicAdd_system(f.err, 1u);
+            break;
+          }
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      item[0] = pass;
+      item[1] = k;
+      item[2] = t;
+    }
+    __syncthreads();  // also: every warp is done with the previous item's ring
+    const int pass = item[0], k = item[1], t = item[2];
+    if (pass < 0) break;
+    const int zt = (t % f.tzn) * QZ, yt = (t / f.tzn) * QY;
+    const int xb = k * f.C, xe = min(a.nx, xb + f.C);
+    if (pass == 0) {
+      el_queue_body<R, 0, SPONGE>(mv, a, zt, yt, xb, xe, smem, !first);
+      __syncthreads();  // the CTA's velocity stores, then one release for all of them
+      if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.flags + (size_t)k * f.T + t),
+                     "r"(f.stamp)
+                     : "memory");
+      }
+    } else {
+      el_queue_body<R, 1, SPONGE>(ms, a, zt, yt, xb, xe, smem, !first);
+    }
+    __syncthreads();  // item[] is rewritten next
+  }
+}
+
+// vz at the receivers after a fused step (the two-pass kernels gather at the
+// start of the stress launch)
+__global__ void el_gather_kernel(const ElStep a) { gather_vz(a); }
+
+// The tensor maps of one pass (velocity: PASS 0, stress: PASS 1).
+template <int R, int PASS>
+static int elq_maps(const fdr_elastic_args* a, ElQMaps* out) {
+  using G = QGeoE<R, PASS>;
+  ElQMaps& maps = *out;
+  int rc = FDR_OK;
+  const int ZBW = QZ + 2 * G::LZ, YBH = QY + 2 * R;
+  if (PASS == 0) {
+    const int win[3] = {SXX, SXY, SXZ};
+    for (int f = 0; f < 3 && rc == FDR_OK; ++f) rc = el_encode(&maps.win[f], a->fields[win[f]], a, QZ, QY);
+    if (rc == FDR_OK) rc = el_encode(&maps.ybox[0], a->fields[SXY], a, QZ, YBH);
+    if (rc == FDR_OK) rc = el_encode(&maps.ybox[1], a->fields[SYY], a, QZ, YBH);
+    if (rc == FDR_OK) rc = el_encode(&maps.zbox[0], a->fields[SXZ], a, ZBW, QY);
+    if (rc == FDR_OK) rc = el_encode(&maps.zbox[1], a->fields[SZZ], a, ZBW, QY);
+    if (rc == FDR_OK) rc = el_encode(&maps.fbox[0], a->fields[SYZ], a, ZBW, YBH);
+    const float* ct[4] = {a->fields[VX], a->fields[VY], a->fields[VZ], a->params[0]};
+    for (int t = 0; t < 4 && rc == FDR_OK; ++t) rc = el_encode(&maps.ctile[t], ct[t], a, QZ, QY);
+  } else {
+    const int win[3] = {VX, VY, VZ};
+    for (int f = 0; f < 3 && rc == FDR_OK; ++f) rc = el_encode(&maps.win[f], a->fields[win[f]], a, QZ, QY);
+    for (int f = 0; f < 3 && rc == FDR_OK; ++f) rc = el_encode(&maps.fbox[f], a->fields[win[f]], a, ZBW, YBH);
+    const float* ct[8] = {a->fields[SXX], a->fields[SYY], a->fields[SZZ], a->fields[SXY],
+                          a->fields[SXZ], a->fields[SYZ], a->params[1], a->params[2]};
+    for (int t = 0; t < 8 && rc == FDR_OK; ++t) rc = el_encode(&maps.ctile[t], ct[t], a, QZ, QY);
+  }
+  return rc;
 }
 
 template <int R, int PASS>
@@ -927,26 +1115,7 @@ static int elq_launch(const ElStep& s, const fdr_elastic_args* a, cudaStream_t s
     *chunk_cache = (a->nx + best_c - 1) / best_c;
   }
   ElQMaps maps;
-  int rc = FDR_OK;
-  const int ZBW = QZ + 2 * G::LZ, YBH = QY + 2 * R;
-  if (PASS == 0) {
-    const int win[3] = {SXX, SXY, SXZ};
-    for (int f = 0; f < 3 && rc == FDR_OK; ++f) rc = el_encode(&maps.win[f], a->fields[win[f]], a, QZ, QY);
-    if (rc == FDR_OK) rc = el_encode(&maps.ybox[0], a->fields[SXY], a, QZ, YBH);
-    if (rc == FDR_OK) rc = el_encode(&maps.ybox[1], a->fields[SYY], a, QZ, YBH);
-    if (rc == FDR_OK) rc = el_encode(&maps.zbox[0], a->fields[SXZ], a, ZBW, QY);
-    if (rc == FDR_OK) rc = el_encode(&maps.zbox[1], a->fields[SZZ], a, ZBW, QY);
-    if (rc == FDR_OK) rc = el_encode(&maps.fbox[0], a->fields[SYZ], a, ZBW, YBH);
-    const float* ct[4] = {a->fields[VX], a->fields[VY], a->fields[VZ], a->params[0]};
-    for (int t = 0; t < 4 && rc == FDR_OK; ++t) rc = el_encode(&maps.ctile[t], ct[t], a, QZ, QY);
-  } else {
-    const int win[3] = {VX, VY, VZ};
-    for (int f = 0; f < 3 && rc == FDR_OK; ++f) rc = el_encode(&maps.win[f], a->fields[win[f]], a, QZ, QY);
-    for (int f = 0; f < 3 && rc == FDR_OK; ++f) rc = el_encode(&maps.fbox[f], a->fields[win[f]], a, ZBW, YBH);
-    const float* ct[8] = {a->fields[SXX], a->fields[SYY], a->fields[SZZ], a->fields[SXY],
-                          a->fields[SXZ], a->fields[SYZ], a->params[1], a->params[2]};
-    for (int t = 0; t < 8 && rc == FDR_OK; ++t) rc = el_encode(&maps.ctile[t], ct[t], a, QZ, QY);
-  }
+  int rc = elq_maps<R, PASS>(a, &maps);
   if (rc != FDR_OK) return rc;
   ElStep t = s;
   t.chunk = *chunk_cache;
@@ -956,8 +1125,203 @@ static int elq_launch(const ElStep& s, const fdr_elastic_args* a, cudaStream_t s
   return FDR_OK;
 }
 
-int el_queue_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, int* chunk_cache) {
+// ---- windowed schedule (experiment, B200FD_EL_WINDOW=C planes) ----
+// The two passes of a step are launched alternately on windows of C x-planes,
+// V(k+1) before S(k), so that the stress launch of window k finds the new
+// velocities and the stresses of its window still in L2 (the two full-grid
+// passes re-read both from HBM: 120 B/pt moved against 84 B/pt algorithmic).
+// V(k+1) before S(k) also keeps the in-place update exact: V(k+1) reads the old
+// stresses of window k's last R planes before S(k) overwrites them, and S(k)
+// needs the new velocities of window k+1's first R planes.  C >= R.
+// B200FD_EL_WINDOW_STREAMS=2 runs the stress launches on a second stream
+// (V(k+2) and S(k) are independent), V(k+LEAD) held until S(k) is done.
+struct ElWindowCtl {
+  int planes = 0, streams = 1, lead = 3, sub = 1;
+  int fuse = 0, fuse_lag = 160;  // B200FD_EL_FUSE (window planes of el_fused), B200FD_EL_FUSE_LAG
+  cudaStream_t aux = nullptr;
+  std::vector<cudaEvent_t> ev_v, ev_s;
+};
+static ElWindowCtl& el_window_ctl() {
+  static ElWindowCtl c;
+  return c;
+}
+// Re-read the knobs (once per run; tests flip them inside one process).
+static void el_window_refresh() {
+  ElWindowCtl& w = el_window_ctl();
+  const char* e = getenv("B200FD_EL_WINDOW");
+  w.planes = e ? atoi(e) : 0;
+  e = getenv("B200FD_EL_WINDOW_STREAMS");
+  w.streams = e ? atoi(e) : 1;
+  e = getenv("B200FD_EL_WINDOW_LEAD");
+  w.lead = e ? std::max(2, atoi(e)) : 3;
+  e = getenv("B200FD_EL_WINDOW_SUB");
+  w.sub = e ? std::max(1, atoi(e)) : 1;
+  e = getenv("B200FD_EL_FUSE");
+  w.fuse = e ? atoi(e) : 0;
+  e = getenv("B200FD_EL_FUSE_LAG");
+  w.fuse_lag = e ? std::max(0, atoi(e)) : 160;
+}
+
+template <int R, int PASS>
+static int elq_fire(const ElQMaps& maps, const ElStep& s, const fdr_elastic_args* a, int x0, int x1,
+                    int sub, cudaStream_t st) {
+  using G = QGeoE<R, PASS>;
+  const bool sponge = s.gx != nullptr;
+  auto kern = sponge ? el_queue<R, PASS, true> : el_queue<R, PASS, false>;
+  int occ = 0, nsm = 0;
+  const int frc = fdr::launch_facts(reinterpret_cast<const void*>(kern), QN, G::SMEM, &occ, &nsm);
+  if (frc != FDR_OK) return frc;
+  ElStep t = s;
+  t.x0 = x0;
+  t.x1 = x1;
+  t.keep_v = 1;
+  t.chunk = (x1 - x0 + sub - 1) / sub;
+  dim3 grid((a->nz + QZ - 1) / QZ, (a->ny + QY - 1) / QY, (x1 - x0 + t.chunk - 1) / t.chunk);
+  kern<<<grid, QN, G::SMEM, st>>>(maps, t);
+  EL_CUDA(cudaGetLastError());
+  return FDR_OK;
+}
+
+template <int R>
+static int el_window_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st) {
+  ElWindowCtl& w = el_window_ctl();
+  const int C = std::max(w.planes, R);
+  const int K = (a->nx + C - 1) / C;
+  const int sub = w.sub;
+  ElQMaps mv, ms;
+  int rc = elq_maps<R, 0>(a, &mv);
+  if (rc == FDR_OK) rc = elq_maps<R, 1>(a, &ms);
+  if (rc != FDR_OK) return rc;
+  auto lo = [&](int k) { return k * C; };
+  auto hi = [&](int k) { return std::min(a->nx, (k + 1) * C); };
+  if (w.streams < 2) {
+    rc = elq_fire<R, 0>(mv, s, a, lo(0), hi(0), sub, st);
+    for (int k = 0; k < K && rc == FDR_OK; ++k) {
+      if (k + 1 < K) rc = elq_fire<R, 0>(mv, s, a, lo(k + 1), hi(k + 1), sub, st);
+      if (rc == FDR_OK) rc = elq_fire<R, 1>(ms, s, a, lo(k), hi(k), sub, st);
+    }
+    return rc;
+  }
+  if (!w.aux) EL_CUDA(cudaStreamCreateWithFlags(&w.aux, cudaStreamNonBlocking));
+  while ((int)w.ev_v.size() < K) {
+    cudaEvent_t e1, e2;
+    EL_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    EL_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+    w.ev_v.push_back(e1);
+    w.ev_s.push_back(e2);
+  }
+  // velocity launches on st, stress launches on aux
+  int s_done = 0;  // stress launches issued so far
+  auto stress = [&](int k) -> int {
+    EL_CUDA(cudaStreamWaitEvent(w.aux, w.ev_v[std::min(k + 1, K - 1)], 0));
+    int r2 = elq_fire<R, 1>(ms, s, a, lo(k), hi(k), sub, w.aux);
+    if (r2 != FDR_OK) return r2;
+    EL_CUDA(cudaEventRecord(w.ev_s[k], w.aux));
+    return FDR_OK;
+  };
+  for (int k = 0; k < K && rc == FDR_OK; ++k) {
+    if (k >= w.lead) EL_CUDA(cudaStreamWaitEvent(st, w.ev_s[k - w.lead], 0));
+    rc = elq_fire<R, 0>(mv, s, a, lo(k), hi(k), sub, st);
+    if (rc != FDR_OK) break;
+    EL_CUDA(cudaEventRecord(w.ev_v[k], st));
+    if (k >= 1) {
+      rc = stress(k - 1);
+      ++s_done;
+    }
+  }
+  if (rc == FDR_OK) rc = stress(K - 1);
+  if (rc == FDR_OK) EL_CUDA(cudaStreamWaitEvent(st, w.ev_s[K - 1], 0));  // join
+  (void)s_done;
+  return rc;
+}
+
+// One time step as one el_fused launch (+ the receiver gather).  Returns
+// FDR_OK with *done = false when the grid is too small for the schedule.
+template <int R>
+static int el_fused_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, ElRunState* rs,
+                         bool* done) {
+  *done = false;
+  ElWindowCtl& w = el_window_ctl();
+  const int C = std::max(w.fuse, R);
+  const int K = (a->nx + C - 1) / C;
+  const int tzn = (a->nz + QZ - 1) / QZ, tyn = (a->ny + QY - 1) / QY;
+  const int T = tzn * tyn;
+  const int lag = std::min(std::max(w.fuse_lag, tzn + 2), T);
+  if (K < 3) return FDR_OK;
+  const bool sponge = s.gx != nullptr;
+  auto kern = sponge ? el_fused<R, true> : el_fused<R, false>;
+  const size_t smem = std::max(QGeoE<R, 0>::SMEM, QGeoE<R, 1>::SMEM);
+  int occ = 0, nsm = 0;
+  int rc = fdr::launch_facts(reinterpret_cast<const void*>(kern), QN, smem, &occ, &nsm);
+  if (rc != FDR_OK) return rc;
+  const size_t nflags = (size_t)K * T;
+  if (!rs->fuse_buf) {
+    EL_CUDA(cudaMallocAsync(&rs->fuse_buf, (nflags + 1) * sizeof(unsigned), st));
+    EL_CUDA(cudaMemsetAsync(rs->fuse_buf, 0, (nflags + 1) * sizeof(unsigned), st));
+    rs->fuse_step = 0;
+  }
+  ElQMaps mv, ms;
+  rc = elq_maps<R, 0>(a, &mv);
+  if (rc == FDR_OK) rc = elq_maps<R, 1>(a, &ms);
+  if (rc != FDR_OK) return rc;
+  int dev = 0;
+  EL_CUDA(cudaGetDevice(&dev));
+  ElFuse f;
+  f.ticket = rs->fuse_buf + nflags;
+  f.flags = rs->fuse_buf;
+  const long long total = 2ll * K * T;
+  const int grid = (int)std::min<long long>(total, (long long)nsm * occ);
+  // every CTA takes one ticket beyond the last item before it exits
+  f.base = (unsigned)((unsigned long long)rs->fuse_step * (unsigned long long)(total + grid));
+  f.stamp = (unsigned)rs->fuse_step + 1u;
+  f.C = C;
+  f.K = K;
+  f.T = T;
+  f.tzn = tzn;
+  f.tyn = tyn;
+  f.lag = lag;
+  const char* wc = getenv("B200FD_WAIT_CYCLES");
+  f.wait_cycles = wc ? atoll(wc) : (1ll << 31);
+  rc = fdr::err_word(dev, &f.err);
+  if (rc != FDR_OK) return rc;
+  ElStep t = s;
+  t.keep_v = 1;
+  kern<<<grid, QN, smem, st>>>(mv, ms, t, f);
+  EL_CUDA(cudaGetLastError());
+  if (t.gather_row >= 0) {
+    el_gather_kernel<<<std::max(1, std::min(64, (t.n_rec + 255) / 256)), 256, 0, st>>>(t);
+    EL_CUDA(cudaGetLastError());
+  }
+  ++rs->fuse_step;
+  *done = true;
+  return FDR_OK;
+}
+
+void el_queue_refresh_knobs() { el_window_refresh(); }
+
+int el_queue_step(const ElStep& s, const fdr_elastic_args* a, cudaStream_t st, ElRunState* rs) {
   int rc = FDR_OK;
+  int* chunk_cache = &rs->chunk;
+  if (el_window_ctl().fuse > 0) {
+    bool done = false;
+    switch (a->order / 2) {
+      case 1: rc = el_fused_step<1>(s, a, st, rs, &done); break;
+      case 2: rc = el_fused_step<2>(s, a, st, rs, &done); break;
+      case 3: rc = el_fused_step<3>(s, a, st, rs, &done); break;
+      case 4: rc = el_fused_step<4>(s, a, st, rs, &done); break;
+      default: return fail(FDR_EINVAL, "elastic queue kernel supports orders 2..8, got %d", a->order);
+    }
+    if (rc != FDR_OK || done) return rc;
+  }
+  if (el_window_ctl().planes > 0) {
+    switch (a->order / 2) {
+      case 1: return el_window_step<1>(s, a, st);
+      case 2: return el_window_step<2>(s, a, st);
+      case 3: return el_window_step<3>(s, a, st);
+      case 4: return el_window_step<4>(s, a, st);
+      default: return fail(FDR_EINVAL, "elastic queue kernel supports orders 2..8, got %d", a->order);
+    }
+  }
   switch (a->order / 2) {
     case 1: rc = elq_launch<1, 0>(s, a, st, chunk_cache); if (rc == FDR_OK) rc = elq_launch<1, 1>(s, a, st, chunk_cache); break;
     case 2: rc = elq_launch<2, 0>(s, a, st, chunk_cache); if (rc == FDR_OK) rc = elq_launch<2, 1>(s, a, st, chunk_cache); break;

@@ -27,6 +27,11 @@ int cuda_fail(cudaError_t e, const char* what);
 // devices never see another device's answer.  FDR_OK or an error code.
 int launch_facts(const void* kern, int threads, size_t smem, int* occ, int* nsm);
 
+// Device pointer (*d) of the host-mapped error word of device `dev`: kernels
+// whose bounded waits time out add to it, and the next fdr_pending_error() /
+// host-buffer run reports FDR_ECUDA (acoustic.cu).
+int err_word(int dev, unsigned** d);
+
 // The driver's cuTensorMapEncodeTiled, resolved once under std::call_once
 // (safe from concurrent host threads); nullptr when the driver lacks it.
 void* tensor_map_encoder();

@@ -158,3 +158,54 @@ def test_gpu_elastic_float64_path_vs_f64_oracle(order, cuda_device):
     assert rel_l2(fld.traces.cpu().numpy()[: cfg.n_t], tr64) < 1e-10
     with pytest.raises(ValidationError):
         elastic.elastic_run(fld, cfg, 1, variant="queue")
+
+
+# The experimental L2-window schedules of the queue path: the
+# library re-reads their knobs at every run, so one process can flip them.
+SCHEDULES = [{"B200FD_EL_WINDOW": "4"}, {"B200FD_EL_WINDOW": "5", "B200FD_EL_WINDOW_STREAMS": "2"},
+             {"B200FD_EL_WINDOW": "8", "B200FD_EL_WINDOW_SUB": "2"}, {"B200FD_EL_FUSE": "4"},
+             {"B200FD_EL_FUSE": "6", "B200FD_EL_FUSE_LAG": "3"}]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("knobs", SCHEDULES, ids=lambda k: "-".join(f"{a[10:]}{b}" for a, b in k.items()))
+@pytest.mark.parametrize("order,dims", [(4, (17, 16, 15)), (8, (33, 30, 37)), (8, (41, 70, 100))])
+def test_gpu_elastic_window_schedules_bitexact(el_mod, monkeypatch, knobs, order, dims):
+    """V(k+1) before S(k) on windows of x-planes (separate launches, or items of
+    the persistent el_fused kernel): same bits as the two full passes."""
+    cfg = small_cfg(order=order, dims=dims, n_t=7)
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    fld = el_mod.ElasticWavefield.allocate(cfg.dims, cfg.halo)
+    el_mod.elastic_run(fld, cfg, variant="queue")
+    from paper_1608_03984_b200 import _lib
+
+    assert _lib.load().fdr_pending_error() == 0
+    st = E.simulate_c(cfg, cfg.params(), elastic_weights_f32(order))
+    for k in FIELDS:
+        assert sha(fld.numpy(k)) == sha(st.interior(k)), k
+    assert (fld.traces.cpu().numpy() == st.traces).all()
+
+
+@pytest.mark.gpu
+def test_gpu_elastic_fused_config5_grid_equals_two_pass(el_mod, monkeypatch):
+    """el_fused on the 320^3 config-5 grid (16000 items per pass and step handed
+    out by tickets over 296 CTAs): 4 steps, bit-identical to the two passes."""
+    cfg = el_mod.config5(n_t=4)
+    rng = np.random.default_rng(7)
+    start = {k: rng.standard_normal(cfg.dims, dtype=np.float32) for k in FIELDS}
+
+    def run():
+        fld = el_mod.ElasticWavefield.allocate(cfg.dims, cfg.halo)
+        for k in FIELDS:
+            fld.set_interior(k, start[k])
+        el_mod.elastic_run(fld, cfg, variant="queue")
+        return {k: sha(fld.numpy(k)) for k in FIELDS}, sha(fld.traces.cpu().numpy())
+
+    ref = run()
+    monkeypatch.setenv("B200FD_EL_FUSE", "4")
+    got = run()
+    from paper_1608_03984_b200 import _lib
+
+    assert _lib.load().fdr_pending_error() == 0
+    assert got == ref
