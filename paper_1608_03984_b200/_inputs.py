@@ -133,6 +133,18 @@ def invalidate_plan(cfg) -> None:
                 pass
 
 
+def to_host(t):
+    """Host numpy copy of a device tensor (or view) in one pass: the device to host
+    copy lands in the result's own memory.  `.cpu().numpy().copy()` allocated and
+    first-touched two host buffers; for a 512^3 float32 level that was 357 ms
+    against 178 ms for the 500 time steps (tools/step_loop_breakdown.py)."""
+    import torch
+
+    out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    torch.from_numpy(out).copy_(t)
+    return out
+
+
 def host_tensor(a):
     """torch.from_numpy for arrays that are only read (copied to the device or
     to pinned memory): write-protected inputs are fine, so torch's warning

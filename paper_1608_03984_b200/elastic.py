@@ -21,7 +21,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._inputs import InputGuard, cached_plan, config_inputs, grow_traces, host_tensor
+from ._inputs import InputGuard, cached_plan, config_inputs, grow_traces, host_tensor, to_host
 from .errors import ValidationError
 from .kernel import Receivers, Source, Sponge, StabilityWarning, row_pitch
 from .stencils import staggered_first_derivative_weights
@@ -165,7 +165,7 @@ class ElasticWavefield:
         return self.fields[0].device
 
     def numpy(self, name: str) -> np.ndarray:
-        return self.fields[FIELDS.index(name)][:, :, : self._dims[2]].cpu().numpy().copy()
+        return to_host(self.fields[FIELDS.index(name)][:, :, : self._dims[2]])
 
     def nonfinite_count(self, name: str = "vz") -> int:
         """NaN/inf values of one field, counted on the device."""

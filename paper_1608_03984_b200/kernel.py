@@ -23,7 +23,8 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._inputs import InputGuard, cached_plan, config_inputs, grow_traces, host_tensor, invalidate_plan  # noqa: F401
+from ._inputs import (InputGuard, cached_plan, config_inputs, grow_traces, host_tensor,  # noqa: F401
+                      invalidate_plan, to_host)
 from .errors import ValidationError
 from .roofline import (
     ACOUSTIC_BYTES_PER_POINT,
@@ -280,7 +281,7 @@ class Wavefield:
 
     def numpy(self, level: int = 2) -> np.ndarray:
         """Host copy of a level's interior (float32, or float64 levels), C order."""
-        return self.interior(level).cpu().numpy().copy()
+        return to_host(self.interior(level))
 
     def set_interior(self, level: int, values) -> None:
         torch = _torch()
@@ -369,9 +370,13 @@ class _DevicePlan:
         else:
             self.m_mode = _lib.M_GRID
             host = np.asarray(cfg.m, dtype=np.float32)  # kernel.py:188
-            self.m_bounds = (float(host.min()), float(host.max()))
             self.m_grid = torch.zeros((nx, ny, pitch), dtype=torch.float32, device=device)
             self.m_grid[:, :, :nz].copy_(host_tensor(np.ascontiguousarray(host)))
+            # bounds of m for the division window, reduced on the device (two
+            # host passes over a 512^3 grid cost ~70 ms of the plan build; NaN
+            # propagates through amin / amax as through numpy's min / max)
+            inner = self.m_grid[:, :, :nz]
+            self.m_bounds = (float(inner.amin().item()), float(inner.amax().item()))
         self.sponge = None
         if cfg.sponge is not None:
             self.sponge = tuple(

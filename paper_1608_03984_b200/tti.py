@@ -27,7 +27,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._inputs import InputGuard, cached_plan, config_inputs, grow_traces, host_tensor
+from ._inputs import InputGuard, cached_plan, config_inputs, grow_traces, host_tensor, to_host
 from .errors import ValidationError
 from .kernel import Receivers, Source, Sponge, StabilityWarning, row_pitch
 from .stencils import first_derivative_weights, second_derivative_weights
@@ -208,7 +208,7 @@ class TTIWavefield:
 
     def numpy(self, field: str = "p", level: int = 2) -> np.ndarray:
         t = (self.p if field == "p" else self.r)[level]
-        return t[:, :, : self._dims[2]].cpu().numpy().copy()
+        return to_host(t[:, :, : self._dims[2]])
 
     def nonfinite_count(self, field: str = "p", level: int = 2) -> int:
         """NaN/inf values of a field's level, counted on the device.
