@@ -3,8 +3,8 @@
 # production kernels (each ncu pass only after the same command exited 0
 # without ncu).
 set -x
-FDR_PARITY_REPORT=gpurun_out/parity_report.json python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
-tail -2 gpurun_out/gpu_tests.log
+FDR_PARITY_REPORT=gpurun_out/parity_report.json python -m pytest tests -q -rs -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
+tail -12 gpurun_out/gpu_tests.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
 B="python bench.py --steps 1 --warmup 1 --no-sweep --no-e2e --no-cpu --no-configs --no-fp64"
