@@ -57,7 +57,7 @@ def parse():
     p.add_argument("--no-sweep", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-steps", type=int, default=5)
+    p.add_argument("--cpu-steps", type=int, default=16)  # ~10 s of CPU work on the 16-core GPU box
     p.add_argument("--no-fp64", action="store_true", help="skip the float64 leg")
     p.add_argument("--no-configs", action="store_true",
                    help="skip the BASELINE configs 1, 3, 4, 5 lines")
