@@ -13,3 +13,6 @@ bash tools/ncu_flops.sh
 ncu --set full --clock-control none --import-source on -k regex:acoustic_queue -s 750 -c 1 -o gpurun_out/full_o8 $B > gpurun_out/ncu2.log 2>&1
 python tools/time_tti.py 6 > gpurun_out/tti6.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:tti_pack -s 4 -c 1 -o gpurun_out/full_tti python tools/time_tti.py 6 > gpurun_out/ncu3.log 2>&1
 ls -la gpurun_out
+# summaries on the box (the reports exceed what comes back comfortably)
+(python tools/ncu_summary.py gpurun_out/full_o8.ncu-rep; python tools/ncu_src_stalls.py gpurun_out/full_o8.ncu-rep) > gpurun_out/r02_ncu_full_bench_o8.txt 2>&1
+(python tools/ncu_summary.py gpurun_out/full_tti.ncu-rep; python tools/ncu_src_stalls.py gpurun_out/full_tti.ncu-rep) > gpurun_out/r02_ncu_full_tti_pack_config4.txt 2>&1
