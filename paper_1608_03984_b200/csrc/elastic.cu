@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/b200fd.h"
@@ -1202,6 +1203,9 @@ static int el_window_step(const ElStep& s, const fdr_elastic_args* a, cudaStream
     }
     return rc;
   }
+  // the helper stream and the event pool are process-wide: one windowed step at a time
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   if (!w.aux) EL_CUDA(cudaStreamCreateWithFlags(&w.aux, cudaStreamNonBlocking));
   while ((int)w.ev_v.size() < K) {
     cudaEvent_t e1, e2;
